@@ -1,0 +1,197 @@
+/*
+ * ntp_b200.h -- C ABI of the B200-native NTP gradient reshard-and-reduce path.
+ *
+ * The reference (arxiv 2504.06095, package `ntpsim`) has no FFI: its boundary
+ * is the Python module API of pkg/src/ntpsim/shardmap.py and
+ * pkg/src/ntpsim/tpnumerics.py.  Each entry point below names the reference
+ * function it replaces (file:line, relative to pkg/src/ntpsim/).  The Python
+ * package paper_2504_06095_b200 binds these with ctypes and re-exposes the
+ * reference's names, argument meaning and ValueError texts; INTEGRATION.md
+ * shows the binding a maintainer of the reference would add.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no torch types.  Device buffers are raw
+ *     CUDA device pointers (local or peer-mapped); `stream` is a cudaStream_t.
+ *   - return value: NTP_OK (0) or a negative status; ntp_last_error() gives
+ *     the message (per thread).  NTP_EINVAL carries the reference's ValueError
+ *     text where the reference has one.
+ *   - all hot-path calls are stream-ordered and asynchronous; no hidden
+ *     allocation happens on the hot path (plans own their device tables).
+ *
+ * Unit-major layout: a rank's gradient buffer stores its columns one after
+ * another; column ("unit") p of a rank occupies elements [off_p, off_p + U).
+ * For an MLP column U = 2*hidden (A column then B row, perfmodel.py:269); for
+ * an attention head U = 4*hidden*head_dim (perfmodel.py:270-272).
+ */
+#ifndef NTP_B200_H
+#define NTP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NTP_ABI_VERSION 1
+
+enum ntp_status {
+  NTP_OK = 0,
+  NTP_EINVAL = -1, /* bad argument: Python raises ValueError(ntp_last_error()) */
+  NTP_ECUDA = -2,  /* CUDA runtime error: Python raises RuntimeError */
+  NTP_ENOMEM = -3,
+  NTP_ESTATE = -4, /* call out of order (e.g. execute before finalize) */
+  NTP_ETIMEOUT = -5 /* a cross-GPU signal did not arrive in time */
+};
+
+enum ntp_dtype { NTP_F32 = 0, NTP_BF16 = 1, NTP_F16 = 2, NTP_F64 = 3 };
+
+/* _reduce, tpnumerics.py:255-260 ("sum" -> a+b, "mean" -> (a+b)/2) plus the
+ * per-replica batch weighting extension w_a*a + w_b*b. */
+enum ntp_op { NTP_OP_SUM = 0, NTP_OP_MEAN = 1, NTP_OP_WEIGHTED = 2 };
+
+/* PRE_SYNC / POST_SYNC, shardmap.py:19-20 */
+enum ntp_direction { NTP_PRE_SYNC = 0, NTP_POST_SYNC = 1 };
+
+const char *ntp_last_error(void);
+int ntp_abi_version(void);
+
+/* ------------------------------------------------------------------------
+ * Shard algebra (host, integer, bit-exact with the reference)
+ * ------------------------------------------------------------------------ */
+
+/* build_shard_map, shardmap.py:141-182 (validation: _validate_triple 132-138).
+ * Writes comp_rank[k] in [0,n1) and sync_rank[k] in [0,n2). */
+int ntp_shard_map(int64_t k, int64_t n1, int64_t n2, int64_t *comp_rank, int64_t *sync_rank);
+
+/* build_reshard_plan, shardmap.py:185-206, flattened: every moving column
+ * becomes one (src, dst, col) triple, sorted by (src, dst, col) -- the
+ * reference's transfer order.  Arrays must hold k entries.  Returns the
+ * number of triples (>= 0) or a negative status. */
+int64_t ntp_reshard_plan(const int64_t *comp_rank, const int64_t *sync_rank, int64_t k,
+                         int64_t n1, int direction, int64_t *src, int64_t *dst, int64_t *col);
+
+/* apply_plan, shardmap.py:209-217: replay n_moves (src, dst, col) triples in
+ * order on ownership[k] in place.  NTP_EINVAL with the reference's message if
+ * a transfer names a column its src does not own. */
+int ntp_apply_plan(int64_t *ownership, int64_t k, const int64_t *src, const int64_t *dst,
+                   const int64_t *col, int64_t n_moves);
+
+/* naive_contiguous_sync_volumes, shardmap.py:220-245: contiguous TP-n2 vs
+ * contiguous TP-n1 interval overlaps.  pairs gets (healthy, overlap) pairs,
+ * reduced shard by reduced shard (capacity 2*(n1+n2)); per_reduced[n2] the
+ * pair count of each reduced shard.  Returns the total pair count. */
+int64_t ntp_naive_overlaps(int64_t k, int64_t n1, int64_t n2, int64_t *pairs,
+                           int64_t *per_reduced);
+
+/* Interval-overlap planner between any two contiguous balanced partitions of k
+ * (TP-n_src -> TP-n_dst), the building block of reconfiguration: writes
+ * (src_rank, dst_rank, start, length) quadruples in ascending start order
+ * (capacity 4*(n_src+n_dst)).  Returns the count. */
+int64_t ntp_interval_overlaps(int64_t k, int64_t n_src, int64_t n_dst, int64_t *quads);
+
+/* attention_head_partition, shardmap.py:248-260. */
+int ntp_head_partition(int64_t heads, int64_t n, int64_t *counts, double *imbalance);
+
+/* ------------------------------------------------------------------------
+ * Copy/reduce plans (host build, device-resident table)
+ * ------------------------------------------------------------------------ */
+
+typedef struct ntp_plan ntp_plan;
+
+typedef struct ntp_plan_stats {
+  int64_t n_units;    /* units added */
+  int64_t n_runs;     /* maximal runs after merging contiguous units */
+  int64_t n_chunks;   /* device work items */
+  int64_t elems;      /* elements per side (sum of unit sizes) */
+  int32_t vectorized; /* 1: every run is 16-byte aligned -> 128-bit path */
+  int32_t max_buf;    /* highest buffer index referenced */
+  int32_t dtype;
+  int32_t device;     /* device the table was uploaded to, -1 if not */
+} ntp_plan_stats;
+
+int ntp_plan_create(ntp_plan **out, int dtype);
+
+/* Append n_units units of unit_elems elements each: unit j pairs side A at
+ * bufs[a_buf[j]] + a_off[j] with side B at bufs[b_buf[j]] + b_off[j]
+ * (element offsets).  For a sync plan A is the healthy replica's copy and B
+ * the reduced replica's (operand order of tpnumerics.py:342-343); for a
+ * reshard plan A is the source and B the destination. */
+int ntp_plan_add_units(ntp_plan *plan, int64_t n_units, int64_t unit_elems, const int32_t *a_buf,
+                       const int64_t *a_off, const int32_t *b_buf, const int64_t *b_off);
+
+/* Merge contiguous units into runs and split runs into device chunks (host). */
+int ntp_plan_finalize(ntp_plan *plan);
+int ntp_plan_stats_get(const ntp_plan *plan, ntp_plan_stats *out);
+
+/* Export the finalized host table: per chunk (a_buf, a_off, b_buf, b_off, len)
+ * in elements; out holds 5*n_chunks int64.  For tests and tooling. */
+int ntp_plan_export(const ntp_plan *plan, int64_t *out);
+
+/* Copy the finalized table to device `device` (cudaMalloc + memcpy). */
+int ntp_plan_upload(ntp_plan *plan, int device);
+void ntp_plan_destroy(ntp_plan *plan);
+
+/* ------------------------------------------------------------------------
+ * Hot path (device, stream-ordered)
+ * ------------------------------------------------------------------------ */
+
+/* nonuniform_grad_sync, tpnumerics.py:289-356 (and the aligned case of
+ * uniform_grad_sync, 263-286, for two replicas): for every unit of the plan
+ *   v = op(A, B)   (fp32 accumulation; fp64 for NTP_F64)
+ *   A = v; B = v   (both replicas end with identical bits, 346-347/355-356)
+ * in one kernel, with no staging buffer: the reference's pre-sync gather,
+ * pairwise reduce and post-sync scatter (323-356) collapse into direct reads
+ * of each unit's two owners.  bufs[n_bufs] may be peer-mapped pointers. */
+int ntp_grad_sync(const ntp_plan *plan, void *const *bufs, int n_bufs, int op, double w_a,
+                  double w_b, void *stream);
+
+/* Reconfiguration copy (no reference function; built from build_reshard_plan
+ * 185-206 / apply_plan 209-217 / contiguous_assignment tpnumerics.py:115-120):
+ * B = A for every unit.  Bit-exact. */
+int ntp_reshard(const ntp_plan *plan, void *const *bufs, int n_bufs, void *stream);
+
+/* uniform_grad_sync, tpnumerics.py:263-286, over R identically laid out local
+ * replicas of n elements: sum in replica order (op SUM), true mean (MEAN) or
+ * sum_r w[r]*x_r (WEIGHTED), written back to all R. */
+int ntp_uniform_sync(void *const *reps, int R, int64_t n, int dtype, int op, const double *w,
+                     void *stream);
+
+/* ------------------------------------------------------------------------
+ * Multi-GPU plumbing: peer memory over NVLink/NVSwitch and device signals
+ * ------------------------------------------------------------------------ */
+
+#define NTP_IPC_HANDLE_BYTES 64
+
+/* Device arena for gradients shared with peers (cudaMalloc'd so it can be
+ * exported with CUDA IPC).  Free with ntp_free. */
+int ntp_alloc(int device, int64_t bytes, void **out);
+int ntp_free(void *ptr);
+int ntp_ipc_get_handle(void *dev_ptr, void *handle_out);
+int ntp_ipc_open(int device, const void *handle, void **dev_ptr_out);
+int ntp_ipc_close(void *dev_ptr);
+
+/* One-sided signalled sync (push design): the computing GPU
+ *   1. waits until every signal word in wait[n_wait] (local memory, written
+ *      by peers with release semantics) is >= epoch,
+ *   2. runs the plan like ntp_grad_sync (reading and writing peer memory),
+ *   3. after all its CTAs finish, stores epoch (release, .sys scope) to every
+ *      word in post[n_post] (peer memory).
+ * spin_ns bounds each wait; on timeout the kernel records NTP_ETIMEOUT in
+ * *status (device int) and exits instead of hanging. */
+int ntp_grad_sync_signaled(const ntp_plan *plan, void *const *bufs, int n_bufs, int op,
+                           double w_a, double w_b, uint64_t *const *wait, int n_wait,
+                           uint64_t *const *post, int n_post, uint64_t epoch,
+                           uint64_t spin_ns, int *status, void *stream);
+
+/* Store epoch to each word in post[] (release, .sys) from a 1-thread kernel. */
+int ntp_signal_post(uint64_t *const *post, int n_post, uint64_t epoch, void *stream);
+
+/* Block the stream until every word in wait[] is >= epoch (bounded spin). */
+int ntp_signal_wait(uint64_t *const *wait, int n_wait, uint64_t epoch, uint64_t spin_ns,
+                    int *status, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NTP_B200_H */

@@ -1,0 +1,616 @@
+// Device side of the NTP gradient reshard-and-reduce (sm_100a).
+//
+// One kernel family covers the whole data path of the reference's
+// nonuniform_grad_sync (pkg/src/ntpsim/tpnumerics.py:289-356): instead of
+// gathering the healthy replica into the reduced layout (323-333), reducing
+// pairwise (338-347) and scattering back (349-356), every unit is read once
+// from each of its two owners -- local HBM or a peer GPU's HBM through an
+// NVLink-mapped pointer -- reduced in fp32 (fp64 for fp64 data) and written
+// once to each owner.  A plan is a table of 16-byte chunk records (see
+// ntp_internal.h) built on the host; a persistent grid walks it.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <mutex>
+#include <string>
+
+#include "ntp_internal.h"
+
+namespace ntp {
+
+static int cuda_fail(cudaError_t e, const char *what) {
+  std::string msg = std::string(what) + ": " + cudaGetErrorString(e);
+  return fail(NTP_ECUDA, msg);
+}
+
+#define NTP_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);  \
+  } while (0)
+
+int device_free(void *p, int device) {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (device >= 0) cudaSetDevice(device);
+  cudaFree(p);
+  if (device >= 0) cudaSetDevice(prev);
+  return NTP_OK;
+}
+
+struct BufTable {
+  char *p[kMaxBufs];
+};
+
+struct SignalArgs {
+  uint64_t *wait[16];
+  uint64_t *post[16];
+  int n_wait, n_post;
+  uint64_t epoch;
+  uint64_t spin_ns;
+  int *status;
+  unsigned int *counter;  // CTA completion counter (device, zeroed)
+};
+
+enum { OP_COPY = 3 };
+constexpr int kThreads = 256;
+constexpr int kUnroll = kChunkVecs / kThreads;  // 4 x 16 B per side per thread
+
+// ---------------------------------------------------------------------------
+// element math
+
+template <typename T>
+struct Acc { using type = float; };
+template <>
+struct Acc<double> { using type = double; };
+
+template <int OP, typename A>
+__device__ __forceinline__ A combine(A a, A b, A wa, A wb) {
+  if constexpr (OP == NTP_OP_SUM) return a + b;                 // tpnumerics.py:257
+  else if constexpr (OP == NTP_OP_MEAN) return (a + b) * A(0.5);  // 259: (a+b)/2.0, exact *0.5
+  else return fma(wa, a, wb * b);                                // w_a*a + w_b*b
+}
+
+template <typename T> __device__ __forceinline__ float2 to_f2(uint32_t w);
+template <>
+__device__ __forceinline__ float2 to_f2<__nv_bfloat16>(uint32_t w) {
+  __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162 *>(&w);
+  return __bfloat1622float2(h);
+}
+template <>
+__device__ __forceinline__ float2 to_f2<__half>(uint32_t w) {
+  __half2 h = *reinterpret_cast<__half2 *>(&w);
+  return __half22float2(h);
+}
+template <typename T> __device__ __forceinline__ uint32_t from_f2(float2 v);
+template <>
+__device__ __forceinline__ uint32_t from_f2<__nv_bfloat16>(float2 v) {
+  __nv_bfloat162 h = __float22bfloat162_rn(v);
+  return *reinterpret_cast<uint32_t *>(&h);
+}
+template <>
+__device__ __forceinline__ uint32_t from_f2<__half>(float2 v) {
+  __half2 h = __float22half2_rn(v);
+  return *reinterpret_cast<uint32_t *>(&h);
+}
+
+// Reduce one 16-byte vector of each side.
+template <typename T, int OP>
+__device__ __forceinline__ uint4 combine_vec(uint4 a, uint4 b, float wa, float wb);
+
+template <int OP>
+__device__ __forceinline__ uint4 combine_vec_f32(uint4 a, uint4 b, float wa, float wb) {
+  uint4 o;
+  o.x = __float_as_uint(combine<OP, float>(__uint_as_float(a.x), __uint_as_float(b.x), wa, wb));
+  o.y = __float_as_uint(combine<OP, float>(__uint_as_float(a.y), __uint_as_float(b.y), wa, wb));
+  o.z = __float_as_uint(combine<OP, float>(__uint_as_float(a.z), __uint_as_float(b.z), wa, wb));
+  o.w = __float_as_uint(combine<OP, float>(__uint_as_float(a.w), __uint_as_float(b.w), wa, wb));
+  return o;
+}
+
+template <typename H, int OP>
+__device__ __forceinline__ uint32_t combine_w16(uint32_t a, uint32_t b, float wa, float wb) {
+  float2 x = to_f2<H>(a), y = to_f2<H>(b);
+  return from_f2<H>(make_float2(combine<OP, float>(x.x, y.x, wa, wb),
+                                combine<OP, float>(x.y, y.y, wa, wb)));
+}
+
+template <typename T, int OP>
+struct VecOp {
+  __device__ static __forceinline__ uint4 run(uint4 a, uint4 b, typename Acc<T>::type wa,
+                                              typename Acc<T>::type wb) {
+    uint4 o;
+    o.x = combine_w16<T, OP>(a.x, b.x, wa, wb);
+    o.y = combine_w16<T, OP>(a.y, b.y, wa, wb);
+    o.z = combine_w16<T, OP>(a.z, b.z, wa, wb);
+    o.w = combine_w16<T, OP>(a.w, b.w, wa, wb);
+    return o;
+  }
+};
+template <int OP>
+struct VecOp<float, OP> {
+  __device__ static __forceinline__ uint4 run(uint4 a, uint4 b, float wa, float wb) {
+    return combine_vec_f32<OP>(a, b, wa, wb);
+  }
+};
+template <int OP>
+struct VecOp<double, OP> {
+  __device__ static __forceinline__ uint4 run(uint4 a, uint4 b, double wa, double wb) {
+    double2 x = *reinterpret_cast<double2 *>(&a), y = *reinterpret_cast<double2 *>(&b);
+    double2 o = make_double2(combine<OP, double>(x.x, y.x, wa, wb),
+                             combine<OP, double>(x.y, y.y, wa, wb));
+    return *reinterpret_cast<uint4 *>(&o);
+  }
+};
+
+// scalar element path (plans whose runs are not 16-byte aligned)
+template <typename T, int OP>
+__device__ __forceinline__ T combine_scalar(T a, T b, typename Acc<T>::type wa,
+                                            typename Acc<T>::type wb) {
+  using A = typename Acc<T>::type;
+  return T(combine<OP, A>(A(a), A(b), wa, wb));
+}
+
+// streaming loads/stores: every byte is touched exactly once per launch
+__device__ __forceinline__ uint4 ld_stream(const uint4 *p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(uint4 *p, uint4 v) { __stcs(p, v); }
+
+// ---------------------------------------------------------------------------
+// cross-GPU signals (release/acquire at system scope)
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t *p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t global_timer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Returns false on timeout (status set).
+__device__ bool wait_signals(uint64_t *const *wait, int n, uint64_t epoch, uint64_t spin_ns,
+                             int *status) {
+  const uint64_t t0 = global_timer_ns();
+  for (int i = 0; i < n; ++i) {
+    while (ld_acquire_sys(wait[i]) < epoch) {
+      if (global_timer_ns() - t0 > spin_ns) {
+        if (status) atomicExch(status, NTP_ETIMEOUT);
+        return false;
+      }
+      __nanosleep(256);
+    }
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// the plan kernels
+
+template <bool kSignaled>
+__device__ __forceinline__ bool cta_prologue(const SignalArgs &sig) {
+  if constexpr (kSignaled) {
+    __shared__ int ok;
+    if (threadIdx.x == 0)
+      ok = wait_signals(sig.wait, sig.n_wait, sig.epoch, sig.spin_ns, sig.status) ? 1 : 0;
+    __syncthreads();
+    return ok != 0;
+  } else {
+    return true;
+  }
+}
+
+template <bool kSignaled>
+__device__ __forceinline__ void cta_epilogue(const SignalArgs &sig) {
+  if constexpr (kSignaled) {
+    __threadfence_system();  // this thread's peer/local stores, system scope
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned int done = atomicAdd(sig.counter, 1u);
+      if (done == gridDim.x - 1) {  // last CTA: every CTA's stores are fenced
+        __threadfence_system();
+        *sig.counter = 0u;
+        for (int i = 0; i < sig.n_post; ++i) st_release_sys(sig.post[i], sig.epoch);
+      }
+    }
+  }
+}
+
+// 128-bit path.  Each CTA walks chunks blockIdx.x, +gridDim.x, ...; the next
+// record is prefetched while the current chunk's loads are in flight.
+template <typename T, int OP, bool kSignaled>
+__global__ void __launch_bounds__(kThreads)
+plan_kernel_vec(const Chunk *__restrict__ chunks, int n_chunks, BufTable bufs,
+                typename Acc<T>::type wa, typename Acc<T>::type wb, SignalArgs sig) {
+  if (!cta_prologue<kSignaled>(sig)) return;
+  const int tid = threadIdx.x;
+  int c = blockIdx.x;
+  uint4 rec = c < n_chunks ? __ldg(reinterpret_cast<const uint4 *>(chunks) + c) : make_uint4(0, 0, 0, 0);
+  for (; c < n_chunks; c += gridDim.x) {
+    const int cn = c + gridDim.x;
+    const uint4 next = cn < n_chunks ? __ldg(reinterpret_cast<const uint4 *>(chunks) + cn) : rec;
+    uint4 *a = reinterpret_cast<uint4 *>(bufs.p[rec.w & 0xffffu]) + rec.x;
+    uint4 *b = reinterpret_cast<uint4 *>(bufs.p[rec.w >> 16]) + rec.y;
+    const int len = (int)rec.z;
+    for (int base = 0; base < len; base += kChunkVecs) {
+      uint4 va[kUnroll], vb[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int i = base + u * kThreads + tid;
+        if (i < len) {
+          va[u] = ld_stream(a + i);
+          if constexpr (OP != OP_COPY) vb[u] = ld_stream(b + i);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int i = base + u * kThreads + tid;
+        if (i < len) {
+          if constexpr (OP == OP_COPY) {
+            st_stream(b + i, va[u]);
+          } else {
+            const uint4 o = VecOp<T, OP>::run(va[u], vb[u], wa, wb);
+            st_stream(a + i, o);
+            st_stream(b + i, o);
+          }
+        }
+      }
+    }
+    rec = next;
+  }
+  cta_epilogue<kSignaled>(sig);
+}
+
+template <typename T, int OP, bool kSignaled>
+__global__ void __launch_bounds__(kThreads)
+plan_kernel_scalar(const Chunk *__restrict__ chunks, int n_chunks, BufTable bufs,
+                   typename Acc<T>::type wa, typename Acc<T>::type wb, SignalArgs sig) {
+  if (!cta_prologue<kSignaled>(sig)) return;
+  for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    const uint4 rec = __ldg(reinterpret_cast<const uint4 *>(chunks) + c);
+    T *a = reinterpret_cast<T *>(bufs.p[rec.w & 0xffffu]) + rec.x;
+    T *b = reinterpret_cast<T *>(bufs.p[rec.w >> 16]) + rec.y;
+    for (int i = threadIdx.x; i < (int)rec.z; i += kThreads) {
+      if constexpr (OP == OP_COPY) {
+        b[i] = a[i];
+      } else {
+        const T o = combine_scalar<T, OP>(a[i], b[i], wa, wb);
+        a[i] = o;
+        b[i] = o;
+      }
+    }
+  }
+  cta_epilogue<kSignaled>(sig);
+}
+
+// uniform_grad_sync over R local replicas (tpnumerics.py:263-286)
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+uniform_kernel(BufTable reps, int R, int64_t n, int op, BufTable wts_unused,
+               typename Acc<T>::type w0, const double *__restrict__ w) {
+  using A = typename Acc<T>::type;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < n; e += stride) {
+    A acc;
+    if (op == NTP_OP_MEAN) {
+      acc = A(0);
+      for (int r = 0; r < R; ++r) acc = acc + A(reinterpret_cast<T *>(reps.p[r])[e]);
+      acc = acc / A(R);
+    } else if (op == NTP_OP_SUM) {
+      acc = A(reinterpret_cast<T *>(reps.p[0])[e]);
+      for (int r = 1; r < R; ++r) acc = acc + A(reinterpret_cast<T *>(reps.p[r])[e]);
+    } else {
+      acc = A(w[0]) * A(reinterpret_cast<T *>(reps.p[0])[e]);
+      for (int r = 1; r < R; ++r) acc = fma(A(w[r]), A(reinterpret_cast<T *>(reps.p[r])[e]), acc);
+    }
+    const T o = T(acc);
+    for (int r = 0; r < R; ++r) reinterpret_cast<T *>(reps.p[r])[e] = o;
+  }
+  (void)wts_unused;
+  (void)w0;
+}
+
+__global__ void signal_post_kernel(SignalArgs sig) {
+  __threadfence_system();
+  for (int i = 0; i < sig.n_post; ++i) st_release_sys(sig.post[i], sig.epoch);
+}
+
+__global__ void signal_wait_kernel(SignalArgs sig) {
+  wait_signals(sig.wait, sig.n_wait, sig.epoch, sig.spin_ns, sig.status);
+}
+
+// ---------------------------------------------------------------------------
+// launch helpers
+
+static int sm_count(int device) {
+  static std::mutex mu;
+  static int cache[64] = {0};
+  std::lock_guard<std::mutex> g(mu);
+  if (device < 0 || device >= 64) return 148;
+  if (!cache[device]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || n <= 0)
+      n = 148;
+    cache[device] = n;
+  }
+  return cache[device];
+}
+
+template <typename K>
+static int grid_for(K kernel, int device, int n_items) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0) != cudaSuccess ||
+      occ <= 0)
+    occ = 4;
+  const int g = sm_count(device) * occ;
+  return n_items < g ? (n_items > 0 ? n_items : 1) : g;
+}
+
+template <typename T, int OP, bool kSig>
+static int launch_plan_t(const ntp_plan *p, const BufTable &bt, double wa, double wb,
+                         const SignalArgs &sig, cudaStream_t s) {
+  using A = typename Acc<T>::type;
+  const int n = (int)p->chunks.size();
+  if (p->vectorized) {
+    auto k = plan_kernel_vec<T, OP, kSig>;
+    k<<<grid_for(k, p->device, n), kThreads, 0, s>>>(p->d_chunks, n, bt, A(wa), A(wb), sig);
+  } else {
+    auto k = plan_kernel_scalar<T, OP, kSig>;
+    k<<<grid_for(k, p->device, n), kThreads, 0, s>>>(p->d_chunks, n, bt, A(wa), A(wb), sig);
+  }
+  return NTP_OK;
+}
+
+template <typename T, bool kSig>
+static int launch_plan_op(const ntp_plan *p, int op, const BufTable &bt, double wa, double wb,
+                          const SignalArgs &sig, cudaStream_t s) {
+  switch (op) {
+    case NTP_OP_SUM: return launch_plan_t<T, NTP_OP_SUM, kSig>(p, bt, wa, wb, sig, s);
+    case NTP_OP_MEAN: return launch_plan_t<T, NTP_OP_MEAN, kSig>(p, bt, wa, wb, sig, s);
+    case NTP_OP_WEIGHTED: return launch_plan_t<T, NTP_OP_WEIGHTED, kSig>(p, bt, wa, wb, sig, s);
+    case OP_COPY: return launch_plan_t<T, OP_COPY, kSig>(p, bt, wa, wb, sig, s);
+    default: return fail(NTP_EINVAL, "unknown reduction op");
+  }
+}
+
+template <bool kSig>
+static int launch_plan(const ntp_plan *p, int op, const BufTable &bt, double wa, double wb,
+                       const SignalArgs &sig, cudaStream_t s) {
+  switch (p->dtype) {
+    case NTP_F32: return launch_plan_op<float, kSig>(p, op, bt, wa, wb, sig, s);
+    case NTP_BF16: return launch_plan_op<__nv_bfloat16, kSig>(p, op, bt, wa, wb, sig, s);
+    case NTP_F16: return launch_plan_op<__half, kSig>(p, op, bt, wa, wb, sig, s);
+    case NTP_F64: return launch_plan_op<double, kSig>(p, op, bt, wa, wb, sig, s);
+    default: return fail(NTP_EINVAL, "unsupported dtype");
+  }
+}
+
+static int check_exec(const ntp_plan *p, void *const *bufs, int n_bufs, BufTable &bt) {
+  if (!p) return fail(NTP_EINVAL, "null plan");
+  if (!p->finalized) return fail(NTP_ESTATE, "plan not finalized");
+  if (p->device < 0 || (!p->d_chunks && !p->chunks.empty()))
+    return fail(NTP_ESTATE, "plan not uploaded to a device");
+  if (n_bufs <= p->max_buf || n_bufs > kMaxBufs)
+    return fail(NTP_EINVAL, "plan references more buffers than were passed");
+  for (int i = 0; i < kMaxBufs; ++i) bt.p[i] = nullptr;
+  for (int i = 0; i < n_bufs; ++i) {
+    bt.p[i] = static_cast<char *>(bufs[i]);
+    if (i <= p->max_buf && !bt.p[i]) return fail(NTP_EINVAL, "null buffer pointer");
+    if (p->vectorized && (reinterpret_cast<uintptr_t>(bt.p[i]) & 15u))
+      return fail(NTP_EINVAL, "buffer not 16-byte aligned for a vectorized plan");
+  }
+  return NTP_OK;
+}
+
+static int set_device(int device) {
+  int cur = -1;
+  NTP_CUDA(cudaGetDevice(&cur));
+  if (cur != device) NTP_CUDA(cudaSetDevice(device));
+  return NTP_OK;
+}
+
+}  // namespace ntp
+
+using namespace ntp;
+
+extern "C" {
+
+int ntp_plan_upload(ntp_plan *p, int device) {
+  if (!p) return fail(NTP_EINVAL, "null plan");
+  if (!p->finalized) return fail(NTP_ESTATE, "plan not finalized");
+  int st = set_device(device);
+  if (st) return st;
+  if (p->d_chunks) {
+    device_free(p->d_chunks, p->device);
+    p->d_chunks = nullptr;
+  }
+  if (p->d_counter) {
+    device_free(p->d_counter, p->device);
+    p->d_counter = nullptr;
+  }
+  p->device = device;
+  NTP_CUDA(cudaMalloc(&p->d_counter, 256));
+  NTP_CUDA(cudaMemset(p->d_counter, 0, 256));
+  if (p->chunks.empty()) return NTP_OK;
+  const size_t bytes = p->chunks.size() * sizeof(Chunk);
+  NTP_CUDA(cudaMalloc(&p->d_chunks, bytes));
+  NTP_CUDA(cudaMemcpy(p->d_chunks, p->chunks.data(), bytes, cudaMemcpyHostToDevice));
+  return NTP_OK;
+}
+
+int ntp_grad_sync(const ntp_plan *p, void *const *bufs, int n_bufs, int op, double w_a,
+                  double w_b, void *stream) {
+  BufTable bt;
+  int st = check_exec(p, bufs, n_bufs, bt);
+  if (st) return st;
+  if (op < NTP_OP_SUM || op > NTP_OP_WEIGHTED) {
+    char buf[64];
+    snprintf(buf, sizeof buf, "unknown reduction op %d", op);
+    return fail(NTP_EINVAL, buf);
+  }
+  if (p->chunks.empty()) return NTP_OK;
+  if ((st = set_device(p->device))) return st;
+  SignalArgs sig{};
+  st = launch_plan<false>(p, op, bt, w_a, w_b, sig, static_cast<cudaStream_t>(stream));
+  if (st) return st;
+  NTP_CUDA(cudaGetLastError());
+  return NTP_OK;
+}
+
+int ntp_reshard(const ntp_plan *p, void *const *bufs, int n_bufs, void *stream) {
+  BufTable bt;
+  int st = check_exec(p, bufs, n_bufs, bt);
+  if (st) return st;
+  if (p->chunks.empty()) return NTP_OK;
+  if ((st = set_device(p->device))) return st;
+  SignalArgs sig{};
+  st = launch_plan<false>(p, OP_COPY, bt, 0.0, 0.0, sig, static_cast<cudaStream_t>(stream));
+  if (st) return st;
+  NTP_CUDA(cudaGetLastError());
+  return NTP_OK;
+}
+
+int ntp_uniform_sync(void *const *reps, int R, int64_t n, int dtype, int op, const double *w,
+                     void *stream) {
+  if (R < 1 || R > kMaxBufs) return fail(NTP_EINVAL, "replica count must be in [1, 64]");
+  if (op < NTP_OP_SUM || op > NTP_OP_WEIGHTED) return fail(NTP_EINVAL, "unknown reduction op");
+  if (n <= 0) return NTP_OK;
+  cudaPointerAttributes attr{};
+  NTP_CUDA(cudaPointerGetAttributes(&attr, reps[0]));
+  int st = set_device(attr.device);
+  if (st) return st;
+  BufTable bt{};
+  for (int r = 0; r < R; ++r) bt.p[r] = static_cast<char *>(reps[r]);
+  double *d_w = nullptr;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (op == NTP_OP_WEIGHTED) {
+    // weights live in a small device buffer owned by the stream's lifetime
+    NTP_CUDA(cudaMallocAsync(&d_w, sizeof(double) * R, s));
+    NTP_CUDA(cudaMemcpyAsync(d_w, w, sizeof(double) * R, cudaMemcpyHostToDevice, s));
+  }
+  const int blocks = (int)std::min<int64_t>((n + kThreads - 1) / kThreads, sm_count(attr.device) * 8);
+  switch (dtype) {
+    case NTP_F32: uniform_kernel<float><<<blocks, kThreads, 0, s>>>(bt, R, n, op, bt, 0.f, d_w); break;
+    case NTP_BF16: uniform_kernel<__nv_bfloat16><<<blocks, kThreads, 0, s>>>(bt, R, n, op, bt, 0.f, d_w); break;
+    case NTP_F16: uniform_kernel<__half><<<blocks, kThreads, 0, s>>>(bt, R, n, op, bt, 0.f, d_w); break;
+    case NTP_F64: uniform_kernel<double><<<blocks, kThreads, 0, s>>>(bt, R, n, op, bt, 0.0, d_w); break;
+    default: return fail(NTP_EINVAL, "unsupported dtype");
+  }
+  NTP_CUDA(cudaGetLastError());
+  if (d_w) NTP_CUDA(cudaFreeAsync(d_w, s));
+  return NTP_OK;
+}
+
+// --------------------------------------------------------------------------
+// multi-GPU plumbing
+
+int ntp_alloc(int device, int64_t bytes, void **out) {
+  if (!out || bytes <= 0) return fail(NTP_EINVAL, "bad allocation request");
+  int st = set_device(device);
+  if (st) return st;
+  NTP_CUDA(cudaMalloc(out, (size_t)bytes));
+  NTP_CUDA(cudaMemset(*out, 0, (size_t)bytes));
+  return NTP_OK;
+}
+
+int ntp_free(void *ptr) {
+  if (!ptr) return NTP_OK;
+  cudaPointerAttributes attr{};
+  NTP_CUDA(cudaPointerGetAttributes(&attr, ptr));
+  int st = set_device(attr.device);
+  if (st) return st;
+  NTP_CUDA(cudaFree(ptr));
+  return NTP_OK;
+}
+
+int ntp_ipc_get_handle(void *dev_ptr, void *handle_out) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == NTP_IPC_HANDLE_BYTES, "ipc handle size");
+  cudaPointerAttributes attr{};
+  NTP_CUDA(cudaPointerGetAttributes(&attr, dev_ptr));
+  int st = set_device(attr.device);
+  if (st) return st;
+  cudaIpcMemHandle_t h;
+  NTP_CUDA(cudaIpcGetMemHandle(&h, dev_ptr));
+  memcpy(handle_out, &h, sizeof h);
+  return NTP_OK;
+}
+
+int ntp_ipc_open(int device, const void *handle, void **dev_ptr_out) {
+  int st = set_device(device);
+  if (st) return st;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof h);
+  NTP_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return NTP_OK;
+}
+
+int ntp_ipc_close(void *dev_ptr) {
+  NTP_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return NTP_OK;
+}
+
+static int fill_signals(SignalArgs &sig, uint64_t *const *wait, int n_wait, uint64_t *const *post,
+                        int n_post, uint64_t epoch, uint64_t spin_ns, int *status) {
+  if (n_wait < 0 || n_wait > 16 || n_post < 0 || n_post > 16)
+    return fail(NTP_EINVAL, "at most 16 wait and 16 post signals");
+  sig = SignalArgs{};
+  for (int i = 0; i < n_wait; ++i) sig.wait[i] = wait[i];
+  for (int i = 0; i < n_post; ++i) sig.post[i] = post[i];
+  sig.n_wait = n_wait;
+  sig.n_post = n_post;
+  sig.epoch = epoch;
+  sig.spin_ns = spin_ns;
+  sig.status = status;
+  return NTP_OK;
+}
+
+int ntp_grad_sync_signaled(const ntp_plan *p, void *const *bufs, int n_bufs, int op, double w_a,
+                           double w_b, uint64_t *const *wait, int n_wait, uint64_t *const *post,
+                           int n_post, uint64_t epoch, uint64_t spin_ns, int *status,
+                           void *stream) {
+  BufTable bt;
+  int st = check_exec(p, bufs, n_bufs, bt);
+  if (st) return st;
+  if (op < NTP_OP_SUM || op > NTP_OP_WEIGHTED) return fail(NTP_EINVAL, "unknown reduction op");
+  if ((st = set_device(p->device))) return st;
+  SignalArgs sig;
+  if ((st = fill_signals(sig, wait, n_wait, post, n_post, epoch, spin_ns, status))) return st;
+  sig.counter = p->d_counter;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (p->chunks.empty()) {
+    signal_wait_kernel<<<1, 1, 0, s>>>(sig);
+    signal_post_kernel<<<1, 1, 0, s>>>(sig);
+  } else {
+    st = launch_plan<true>(p, op, bt, w_a, w_b, sig, s);
+    if (st) return st;
+  }
+  NTP_CUDA(cudaGetLastError());
+  return NTP_OK;
+}
+
+int ntp_signal_post(uint64_t *const *post, int n_post, uint64_t epoch, void *stream) {
+  SignalArgs sig;
+  int st = fill_signals(sig, nullptr, 0, post, n_post, epoch, 0, nullptr);
+  if (st) return st;
+  signal_post_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(sig);
+  NTP_CUDA(cudaGetLastError());
+  return NTP_OK;
+}
+
+int ntp_signal_wait(uint64_t *const *wait, int n_wait, uint64_t epoch, uint64_t spin_ns,
+                    int *status, void *stream) {
+  SignalArgs sig;
+  int st = fill_signals(sig, wait, n_wait, nullptr, 0, epoch, spin_ns, status);
+  if (st) return st;
+  signal_wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(sig);
+  NTP_CUDA(cudaGetLastError());
+  return NTP_OK;
+}
+
+}  // extern "C"
