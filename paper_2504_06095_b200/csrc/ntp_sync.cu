@@ -66,11 +66,18 @@ struct Acc { using type = float; };
 template <>
 struct Acc<double> { using type = double; };
 
+// Explicitly rounded operations: no FMA contraction, so the device result is
+// the IEEE evaluation of the written expression (identical to the oracle's).
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+
 template <int OP, typename A>
 __device__ __forceinline__ A combine(A a, A b, A wa, A wb) {
-  if constexpr (OP == NTP_OP_SUM) return a + b;                 // tpnumerics.py:257
-  else if constexpr (OP == NTP_OP_MEAN) return (a + b) * A(0.5);  // 259: (a+b)/2.0, exact *0.5
-  else return fma(wa, a, wb * b);                                // w_a*a + w_b*b
+  if constexpr (OP == NTP_OP_SUM) return add_rn(a, b);                      // tpnumerics.py:257
+  else if constexpr (OP == NTP_OP_MEAN) return mul_rn(add_rn(a, b), A(0.5));  // 259: (a+b)/2.0 (exact *0.5)
+  else return add_rn(mul_rn(wa, a), mul_rn(wb, b));                       // w_a*a + w_b*b
 }
 
 template <typename T> __device__ __forceinline__ float2 to_f2(uint32_t w);
@@ -300,14 +307,15 @@ uniform_kernel(BufTable reps, int R, int64_t n, int op, BufTable wts_unused,
     A acc;
     if (op == NTP_OP_MEAN) {
       acc = A(0);
-      for (int r = 0; r < R; ++r) acc = acc + A(reinterpret_cast<T *>(reps.p[r])[e]);
+      for (int r = 0; r < R; ++r) acc = add_rn(acc, A(reinterpret_cast<T *>(reps.p[r])[e]));
       acc = acc / A(R);
     } else if (op == NTP_OP_SUM) {
       acc = A(reinterpret_cast<T *>(reps.p[0])[e]);
-      for (int r = 1; r < R; ++r) acc = acc + A(reinterpret_cast<T *>(reps.p[r])[e]);
+      for (int r = 1; r < R; ++r) acc = add_rn(acc, A(reinterpret_cast<T *>(reps.p[r])[e]));
     } else {
-      acc = A(w[0]) * A(reinterpret_cast<T *>(reps.p[0])[e]);
-      for (int r = 1; r < R; ++r) acc = fma(A(w[r]), A(reinterpret_cast<T *>(reps.p[r])[e]), acc);
+      acc = mul_rn(A(w[0]), A(reinterpret_cast<T *>(reps.p[0])[e]));
+      for (int r = 1; r < R; ++r)
+        acc = add_rn(acc, mul_rn(A(w[r]), A(reinterpret_cast<T *>(reps.p[r])[e])));
     }
     const T o = T(acc);
     for (int r = 0; r < R; ++r) reinterpret_cast<T *>(reps.p[r])[e] = o;

@@ -1,0 +1,166 @@
+"""Host logic of the multi-GPU sync (paper_2504_06095_b200/dist.py) on CPU:
+placement, per-process plans, IPC-handle exchange over a real gloo process
+group (world size 2), and signal wiring.  Device calls are replaced by a fake;
+the per-process chunk tables are replayed on numpy arenas and must reproduce
+the oracle's nonuniform sync of the whole layout."""
+
+import os
+import pickle
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+from paper_2504_06095_b200 import dist as D
+from paper_2504_06095_b200.workloads import ModelShape, pair_layout
+
+SHAPE = ModelShape("tiny", hidden=16, ffn=96, heads=4, layers=3)
+
+
+class FakeOps:
+    """Pointers are (rank, n) pairs encoded as ints; handles are pickles."""
+
+    def __init__(self, rank):
+        self.rank, self.n = rank, 0
+
+    def alloc(self, nbytes):
+        self.n += 1
+        return (self.rank << 32) | self.n
+
+    def handle(self, ptr):
+        return pickle.dumps(ptr).ljust(64, b"\0")
+
+    def open(self, handle):
+        return pickle.loads(handle.rstrip(b"\0") if handle[-1:] == b"\0" else handle)
+
+    def close(self, ptr):
+        pass
+
+    def free(self, ptr):
+        pass
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n1, n2, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lay = pair_layout(SHAPE, n1, n2)
+    plc = D.Placement.default(world, n1, n2)
+    g = D.NtpSyncGroup(lay, plc, torch.float32, device=0, ops=FakeOps(rank))
+    tab = g.plan.export() if g.plan is not None else np.zeros((0, 5), dtype=np.int64)
+    slots = sorted(g.slot_ptr)
+    q.put((rank, tab, slots, g.wait_ready, g.post_done, g.post_ready, g.wait_done,
+           g.ready_from, g.done_to, g.done_from, g.sig))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _run_world(world, n1, n2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n1, n2, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return {o[0]: o[1:] for o in out}
+
+
+def _replay(lay, per_rank, w=(4 / 7, 3 / 7), seed=0):
+    rng = np.random.default_rng(seed)
+    arenas = [rng.standard_normal(e) for e in list(lay.h_elems) + list(lay.r_elems)]
+    want_h = [a.copy() for a in arenas[:lay.n1]]
+    want_r = [a.copy() for a in arenas[lay.n1:]]
+    covered = [np.zeros(len(a), dtype=np.int32) for a in arenas]
+    for rank, (tab, slots, *_rest) in per_rank.items():
+        for ab, ao, bb, bo, ln in tab:
+            A, B = arenas[slots[ab]], arenas[slots[bb]]
+            v = w[0] * A[ao:ao + ln] + w[1] * B[bo:bo + ln]
+            A[ao:ao + ln] = v
+            B[bo:bo + ln] = v
+            covered[slots[ab]][ao:ao + ln] += 1
+            covered[slots[bb]][bo:bo + ln] += 1
+    for c in covered:
+        assert (c == 1).all()
+    # oracle, segment by segment
+    for k, unit, hc, rc, hb, rb in lay.segs:
+        comp = np.empty(k, dtype=np.int64)
+        sync = np.empty(k, dtype=np.int64)
+        for r, c in enumerate(hc):
+            comp[c] = r
+        for r, c in enumerate(rc):
+            sync[c] = r
+        hv = [want_h[r][hb[r]:hb[r] + len(c) * unit].copy() for r, c in enumerate(hc)]
+        rv = [want_r[r][rb[r]:rb[r] + len(c) * unit].copy() for r, c in enumerate(rc)]
+        O.nonuniform_sync(comp, sync, hc, rc, hv, rv, unit, op=O.OP_WEIGHTED, weights=w)
+        for r, c in enumerate(hc):
+            want_h[r][hb[r]:hb[r] + len(c) * unit] = hv[r]
+        for r, c in enumerate(rc):
+            want_r[r][rb[r]:rb[r] + len(c) * unit] = rv[r]
+    for got, want in zip(arenas, want_h + want_r):
+        np.testing.assert_allclose(got, want, rtol=1e-14, atol=1e-14)
+
+
+def _check_wiring(per_rank):
+    ready_posts = set()
+    ready_waits = set()
+    done_posts = set()
+    done_waits = set()
+    for rank, (_t, _s, _wr, _pd, _pr, _wd, ready_from, done_to, done_from, _sig) in per_rank.items():
+        ready_waits |= {(p, rank) for p in ready_from}
+        done_posts |= {(rank, p) for p in done_to}
+        ready_posts |= {(rank, p) for p in done_from}   # healthy posts ready to its reduced peers
+        done_waits |= {(p, rank) for p in done_from}
+    assert ready_posts == ready_waits
+    assert done_posts == done_waits
+
+
+@pytest.mark.parametrize("n1,n2", [(4, 3), (2, 1)])
+def test_gloo_world2_plans_and_wiring(n1, n2):
+    per_rank = _run_world(2, n1, n2)
+    lay = pair_layout(SHAPE, n1, n2)
+    _replay(lay, per_rank)
+    _check_wiring(per_rank)
+    # world 2: healthy replica on rank 0, reduced on rank 1; rank 1 does all the work
+    assert len(per_rank[0][0]) == 0 and len(per_rank[1][0]) > 0
+
+
+def test_placements():
+    assert D.Placement.default(8, 4, 3) == D.Placement(4, 3, (0, 1, 2, 3), (4, 5, 6))
+    assert D.Placement.default(1, 4, 3) == D.Placement(4, 3, (0,) * 4, (0,) * 3)
+    assert D.Placement.default(2, 4, 3) == D.Placement(4, 3, (0,) * 4, (1,) * 3)
+    p = D.Placement.default(4, 2, 1)
+    assert p.h_proc == (0, 1) and p.r_proc == (2,)
+    p = D.Placement.default(4, 4, 3)
+    assert set(p.h_proc) | set(p.r_proc) == {0, 1, 2, 3}
+
+
+@pytest.mark.parametrize("world,n1,n2", [(8, 4, 3), (4, 2, 1), (3, 2, 1), (8, 4, 2)])
+def test_single_process_emulation_of_larger_worlds(world, n1, n2):
+    """Per-process unit selection for worlds we cannot spawn cheaply: every
+    unit is computed by exactly one process, and the union equals the oracle."""
+    lay = pair_layout(SHAPE, n1, n2)
+    plc = D.Placement.default(world, n1, n2)
+    per_rank = {}
+    for rank in range(world):
+        units, touched = D.process_plan_units(lay, plc, rank)
+        rows = []
+        for unit, hs, ho, rs, ro in units:
+            rows += [(h, a, r, b, unit) for h, a, r, b in zip(hs, ho, rs, ro)]
+        tab = np.array(rows, dtype=np.int64).reshape(-1, 5)
+        per_rank[rank] = (tab, list(range(n1 + n2)))
+    _replay(lay, per_rank)
