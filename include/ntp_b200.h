@@ -55,6 +55,16 @@ enum ntp_direction { NTP_PRE_SYNC = 0, NTP_POST_SYNC = 1 };
 const char *ntp_last_error(void);
 int ntp_abi_version(void);
 
+/* Process-wide tuning knobs (no reference counterpart). */
+enum ntp_option { NTP_OPT_SYNC_KERNEL = 0 };
+enum ntp_sync_kernel {
+  NTP_KERNEL_LDG = 1,   /* 128-bit register-staged loads/stores (default) */
+  NTP_KERNEL_BULK = 2,  /* TMA bulk copies through shared memory, 4 stages, 1 CTA/SM */
+  NTP_KERNEL_BULK2 = 3  /* TMA bulk copies, 3 stages, 2 CTAs/SM */
+};
+int ntp_set_option(int option, int64_t value);
+int64_t ntp_get_option(int option);
+
 /* ------------------------------------------------------------------------
  * Shard algebra (host, integer, bit-exact with the reference)
  * ------------------------------------------------------------------------ */

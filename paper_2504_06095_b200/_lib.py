@@ -40,6 +40,8 @@ class PlanStats(ctypes.Structure):
 SIGNATURES = {
     "ntp_last_error": (ctypes.c_char_p, []),
     "ntp_abi_version": (ctypes.c_int, []),
+    "ntp_set_option": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64]),
+    "ntp_get_option": (ctypes.c_int64, [ctypes.c_int]),
     "ntp_shard_map": (ctypes.c_int, [ctypes.c_int64] * 3 + [_i64p, _i64p]),
     "ntp_reshard_plan": (ctypes.c_int64, [_i64p, _i64p, ctypes.c_int64, ctypes.c_int64,
                                           ctypes.c_int, _i64p, _i64p, _i64p]),

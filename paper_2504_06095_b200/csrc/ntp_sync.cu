@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <atomic>
 #include <mutex>
 #include <string>
 
@@ -274,6 +275,146 @@ plan_kernel_vec(const Chunk *__restrict__ chunks, int n_chunks, BufTable bufs,
   cta_epilogue<kSignaled>(sig);
 }
 
+// ---------------------------------------------------------------------------
+// TMA bulk-copy variant: a producer warp streams both sides of each chunk into
+// shared memory with cp.async.bulk (mbarrier complete_tx), four consumer warps
+// reduce in shared memory, and one consumer thread writes the result back to
+// both owners with cp.async.bulk stores.  kStages chunk-sized stages keep
+// ~kStages*32 KiB of loads in flight per CTA without register staging.
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void *smem_dst, const void *gsrc, uint32_t bytes,
+                                          uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void *gdst, const void *smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+constexpr int kBulkConsumers = 128;                 // 4 consumer warps
+constexpr int kBulkThreads = kBulkConsumers + 32;   // + 1 producer warp
+constexpr int kChunkBytes = kChunkVecs * 16;        // 16 KiB per side per stage
+
+template <int kStages>
+struct BulkSmem {
+  uint4 a[kStages][kChunkVecs];
+  uint4 b[kStages][kChunkVecs];
+  uint64_t full[kStages];
+  uint64_t empty[kStages];
+};
+
+template <typename T, int OP, int kStages>
+__global__ void __launch_bounds__(kBulkThreads, 1)
+plan_kernel_bulk(const Chunk *__restrict__ chunks, int n_chunks, BufTable bufs,
+                 typename Acc<T>::type wa, typename Acc<T>::type wb) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  auto &sm = *reinterpret_cast<BulkSmem<kStages> *>(smem_raw);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint4 *recs = reinterpret_cast<const uint4 *>(chunks);
+  if (warp == kBulkConsumers / 32) {
+    // ---- producer: one elected lane issues the bulk loads ----
+    if ((tid & 31) == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+        const uint4 rec = __ldg(recs + c);
+        const uint32_t bytes = rec.z * 16u;
+        mbar_wait(&sm.empty[stage], phase ^ 1u);
+        const uint4 *ga = reinterpret_cast<const uint4 *>(bufs.p[rec.w & 0xffffu]) + rec.x;
+        const uint4 *gb = reinterpret_cast<const uint4 *>(bufs.p[rec.w >> 16]) + rec.y;
+        if constexpr (OP == OP_COPY) {
+          mbar_expect_tx(&sm.full[stage], bytes);
+          bulk_load(sm.a[stage], ga, bytes, &sm.full[stage]);
+        } else {
+          mbar_expect_tx(&sm.full[stage], 2u * bytes);
+          bulk_load(sm.a[stage], ga, bytes, &sm.full[stage]);
+          bulk_load(sm.b[stage], gb, bytes, &sm.full[stage]);
+        }
+        if (++stage == kStages) { stage = 0; phase ^= 1u; }
+      }
+    }
+    return;
+  }
+  // ---- consumers ----
+  int stage = 0, prev_stage = -1;
+  uint32_t phase = 0;
+  for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    const uint4 rec = __ldg(recs + c);
+    const int len = (int)rec.z;
+    mbar_wait(&sm.full[stage], phase);
+    if constexpr (OP != OP_COPY) {
+      for (int i = tid; i < len; i += kBulkConsumers)
+        sm.a[stage][i] = VecOp<T, OP>::run(sm.a[stage][i], sm.b[stage][i], wa, wb);
+      fence_proxy_async_smem();
+    }
+    named_bar_sync(1, kBulkConsumers);
+    if (tid == 0) {
+      uint4 *ga = reinterpret_cast<uint4 *>(bufs.p[rec.w & 0xffffu]) + rec.x;
+      uint4 *gb = reinterpret_cast<uint4 *>(bufs.p[rec.w >> 16]) + rec.y;
+      if constexpr (OP != OP_COPY) bulk_store(ga, sm.a[stage], rec.z * 16u);
+      bulk_store(gb, sm.a[stage], rec.z * 16u);
+      bulk_commit();
+      // the previous stage's stores have finished reading shared memory
+      bulk_wait_read<1>();
+      if (prev_stage >= 0) mbar_arrive(&sm.empty[prev_stage]);
+    }
+    prev_stage = stage;
+    if (++stage == kStages) { stage = 0; phase ^= 1u; }
+  }
+  if (tid == 0) bulk_wait_all();
+}
+
 template <typename T, int OP, bool kSignaled>
 __global__ void __launch_bounds__(kThreads)
 plan_kernel_scalar(const Chunk *__restrict__ chunks, int n_chunks, BufTable bufs,
@@ -360,11 +501,35 @@ static int grid_for(K kernel, int device, int n_items) {
   return n_items < g ? (n_items > 0 ? n_items : 1) : g;
 }
 
+static std::atomic<int> g_sync_kernel{NTP_KERNEL_LDG};
+
+template <typename T, int OP, int kStages>
+static int launch_bulk(const ntp_plan *p, const BufTable &bt, typename Acc<T>::type wa,
+                       typename Acc<T>::type wb, int ctas_per_sm, cudaStream_t s) {
+  auto k = plan_kernel_bulk<T, OP, kStages>;
+  const int smem = (int)sizeof(BulkSmem<kStages>);
+  static std::once_flag once[64];
+  const int dev = p->device >= 0 && p->device < 64 ? p->device : 0;
+  std::call_once(once[dev], [&] {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  });
+  const int n = (int)p->chunks.size();
+  int grid = sm_count(p->device) * ctas_per_sm;
+  if (n < grid) grid = n > 0 ? n : 1;
+  k<<<grid, kBulkThreads, smem, s>>>(p->d_chunks, n, bt, wa, wb);
+  return NTP_OK;
+}
+
 template <typename T, int OP, bool kSig>
 static int launch_plan_t(const ntp_plan *p, const BufTable &bt, double wa, double wb,
                          const SignalArgs &sig, cudaStream_t s) {
   using A = typename Acc<T>::type;
   const int n = (int)p->chunks.size();
+  const int variant = g_sync_kernel.load();
+  if (p->vectorized && !kSig && (variant == NTP_KERNEL_BULK || variant == NTP_KERNEL_BULK2)) {
+    if (variant == NTP_KERNEL_BULK) return launch_bulk<T, OP, 4>(p, bt, A(wa), A(wb), 1, s);
+    return launch_bulk<T, OP, 3>(p, bt, A(wa), A(wb), 2, s);
+  }
   if (p->vectorized) {
     auto k = plan_kernel_vec<T, OP, kSig>;
     k<<<grid_for(k, p->device, n), kThreads, 0, s>>>(p->d_chunks, n, bt, A(wa), A(wb), sig);
@@ -428,6 +593,19 @@ static int set_device(int device) {
 using namespace ntp;
 
 extern "C" {
+
+int ntp_set_option(int option, int64_t value) {
+  if (option != NTP_OPT_SYNC_KERNEL) return fail(NTP_EINVAL, "unknown option");
+  if (value < NTP_KERNEL_LDG || value > NTP_KERNEL_BULK2)
+    return fail(NTP_EINVAL, "unknown sync kernel variant");
+  g_sync_kernel.store((int)value);
+  return NTP_OK;
+}
+
+int64_t ntp_get_option(int option) {
+  if (option != NTP_OPT_SYNC_KERNEL) return fail(NTP_EINVAL, "unknown option");
+  return g_sync_kernel.load();
+}
 
 int ntp_plan_upload(ntp_plan *p, int device) {
   if (!p) return fail(NTP_EINVAL, "null plan");

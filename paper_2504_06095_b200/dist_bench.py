@@ -1,0 +1,164 @@
+"""bench.py's N>1 arm: one process per GPU (torchrun), NVLink peer-memory sync.
+
+The same workload as N=1 (gpt-1.3b, DP=2 TP4+TP3, bf16), with the 7 logical
+ranks placed on the N GPUs by ``Placement.default`` (N>=8: one GPU per logical
+rank, GPU 7 idle as the failed one; N=2: healthy replica on GPU 0, reduced on
+GPU 1; N=4: 2+2 GPUs).  Each rank device-times its K steps with CUDA events;
+rank 0 reports the max over ranks.
+"""
+
+from __future__ import annotations
+
+import os
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .dist import NtpSyncGroup, Placement
+from .workloads import SHAPES, busiest_bytes, pair_layout
+
+
+def _max(x: float) -> float:
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run(args):
+    from bench import METRIC, W_H, W_R, ClockSampler, peaks  # noqa: I001 (repo root on sys.path)
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    _lib.load()
+    shape = SHAPES[args.workload]
+    n1, n2 = 4, 3
+    lay = pair_layout(shape, n1, n2)
+    plc = Placement.default(world, n1, n2)
+    dtype, eb = torch.bfloat16, 2
+    grp = NtpSyncGroup(lay, plc, dtype, device=local).upload()
+    gen = torch.Generator(device="cuda").manual_seed(1000 + rank)
+    for s in grp.hosted:
+        a = grp.arena(s)
+        a.copy_(torch.randn(a.numel(), generator=gen, device="cuda").to(dtype))
+    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    dist.barrier()
+    for _ in range(max(args.warmup, 3)):
+        grp.step(W_H, W_R, stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    if grp.status() != 0:
+        raise RuntimeError(f"rank {rank}: signal timeout during warm-up")
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks.mark("t0")
+    e0.record(stream)
+    for _ in range(args.steps):
+        grp.step(W_H, W_R, stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks.mark("t1")
+    dist.barrier()
+    clk = clocks.stop()
+    ms = _max(e0.elapsed_time(e1) / args.steps)
+    kernel_ms = ms
+    if grp.status() != 0:
+        raise RuntimeError(f"rank {rank}: signal timeout")
+    S = lay.elems
+    B = busiest_bytes_for(lay, plc, eb)
+    pk = peaks()
+    achieved = B / (ms * 1e-3) / 1e9
+    out = None
+    e2e = run_e2e(args, grp, lay, dtype, eb)
+    if rank == 0:
+        out = {"metric": METRIC, "value": round(S * eb / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+               "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+               "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "bf16",
+               "data": "synthetic (N(0,1) bf16 gradients)",
+               "config": {"workload": f"{shape.name} DP=2 TP4+TP3 full-step grad sync over NVLink",
+                          "placement_healthy": list(plc.h_proc),
+                          "placement_reduced": list(plc.r_proc),
+                          "grad_bytes_per_replica": S * eb,
+                          "busiest_gpu_bytes_per_direction": B,
+                          "weights": [round(W_H, 6), round(W_R, 6)],
+                          "l2": "inputs >> L2"},
+               "roofline": {"bound": "nvlink", "kernel": "ntp::plan_kernel_vec<bf16,weighted,signaled>",
+                            "achieved": round(achieved, 1), "peak": pk["nvlink_gbs"],
+                            "peak_src": "measured peer copy 770 GB/s/direction (B200_PROFILING.md)",
+                            "unit": "GB/s", "frac": round(achieved / pk["nvlink_gbs"], 4),
+                            "algorithmic_bytes_per_launch": B, "traffic": None,
+                            "kernel_ms": round(kernel_ms, 4)},
+               "gpu_launches": args.steps * _launches_per_step(grp),
+               "clocks": clk, "e2e": e2e}
+    dist.barrier()
+    grp.close()
+    return out
+
+
+def busiest_bytes_for(lay, plc: Placement, eb: int) -> int:
+    """Busiest GPU's one-direction NVLink bytes for this placement: elements it
+    hosts whose partner copy lives on another GPU."""
+    worst = 0
+    for rank in set(plc.h_proc) | set(plc.r_proc):
+        remote = 0
+        for k, unit, hc, rc, hb, rbase in lay.segs:
+            comp = np.empty(k, dtype=np.int64)
+            for r, c in enumerate(hc):
+                comp[c] = r
+            for j, c in enumerate(rc):
+                hp = np.array(plc.h_proc)[comp[c]]
+                rp = plc.r_proc[j]
+                if rp == rank:
+                    remote += int((hp != rank).sum()) * unit
+                else:
+                    remote += int(((hp == rank)).sum()) * unit
+        worst = max(worst, remote)
+    return worst * eb
+
+
+def _launches_per_step(grp) -> int:
+    return int(grp.plan is not None) + int(bool(grp.post_ready)) + int(bool(grp.wait_done))
+
+
+def run_e2e(args, grp, lay, dtype, eb):
+    """Per rank: pinned host arenas -> device, sync, device -> host; max over ranks."""
+    host = {s: torch.empty(grp.slot_elems[s], dtype=dtype).pin_memory() for s in grp.hosted}
+    dev = {s: grp.arena(s) for s in grp.hosted}
+    stream = torch.cuda.current_stream()
+    steps = max(2, min(args.e2e_steps, args.steps))
+
+    def one():
+        for s in grp.hosted:
+            dev[s].copy_(host[s], non_blocking=True)
+        grp.step(4 / 7, 3 / 7, stream)
+        for s in grp.hosted:
+            host[s].copy_(dev[s], non_blocking=True)
+
+    one()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(steps):
+        one()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = _max(e0.elapsed_time(e1) / steps)
+    nbytes = sum(grp.slot_elems[s] for s in grp.hosted) * eb
+    h2d = int(_max(float(nbytes)))
+    return {"value": round(lay.elems * eb / (ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+            "ms_per_step": round(ms, 3), "steps": steps,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h2d,
+            "note": "per-rank max; every rank copies its own arenas over its own PCIe link",
+            "wall_ms_per_step": round((time.perf_counter() - t0) * 1e3 / steps, 3)}

@@ -1,0 +1,93 @@
+"""Multi-GPU parity check (run under torchrun): every rank syncs its hosted
+arenas through NtpSyncGroup (IPC peer memory + device signals); rank 0 gathers
+all arenas and compares them with the oracle's fp64 nonuniform sync.
+
+    torchrun --nproc-per-node N scripts/dist_check.py [n1 n2 dtype steps]
+"""
+
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from oracle import oracle as O  # noqa: E402
+from paper_2504_06095_b200.dist import NtpSyncGroup, Placement  # noqa: E402
+from paper_2504_06095_b200.workloads import ModelShape, pair_layout  # noqa: E402
+
+DT = {"f32": torch.float32, "bf16": torch.bfloat16, "f64": torch.float64}
+TOL = {"f32": 1e-6, "bf16": 2e-2, "f64": 0.0}
+
+
+def main():
+    n1 = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+    n2 = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+    dname = sys.argv[3] if len(sys.argv) > 3 else "f32"
+    steps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    shape = ModelShape("check", hidden=256, ffn=1000, heads=8, layers=3)
+    lay = pair_layout(shape, n1, n2)
+    plc = Placement.default(world, n1, n2)
+    dtype = DT[dname]
+    grp = NtpSyncGroup(lay, plc, dtype, device=local).upload()
+    rng = np.random.default_rng(0)
+    init = [rng.standard_normal(e) for e in list(lay.h_elems) + list(lay.r_elems)]
+    init = [torch.from_numpy(a).to(dtype).double().numpy() for a in init]  # representable
+    for s in grp.hosted:
+        grp.arena(s).copy_(torch.from_numpy(init[s]).to(dtype))
+    torch.cuda.synchronize()
+    dist.barrier()
+    w = (4 / 7, 3 / 7)
+    for _ in range(steps):
+        grp.step(*w)
+    torch.cuda.synchronize()
+    dist.barrier()
+    assert grp.status() == 0, "signal timeout"
+    mine = {s: grp.arena(s).double().cpu().numpy() for s in grp.hosted}
+    allv = [None] * world
+    dist.all_gather_object(allv, mine)
+    ok = True
+    if rank == 0:
+        got = {}
+        for d in allv:
+            got.update(d)
+        want = [a.copy() for a in init]
+        for _ in range(steps):
+            for k, unit, hc, rc, hb, rb in lay.segs:
+                comp = np.empty(k, dtype=np.int64)
+                sync = np.empty(k, dtype=np.int64)
+                for r, c in enumerate(hc):
+                    comp[c] = r
+                for r, c in enumerate(rc):
+                    sync[c] = r
+                hv = [want[r][hb[r]:hb[r] + len(c) * unit].copy() for r, c in enumerate(hc)]
+                rv = [want[n1 + r][rb[r]:rb[r] + len(c) * unit].copy() for r, c in enumerate(rc)]
+                O.nonuniform_sync(comp, sync, hc, rc, hv, rv, unit, op=O.OP_WEIGHTED, weights=w)
+                for r, c in enumerate(hc):
+                    want[r][hb[r]:hb[r] + len(c) * unit] = hv[r]
+                for r, c in enumerate(rc):
+                    want[n1 + r][rb[r]:rb[r] + len(c) * unit] = rv[r]
+            # the device result of each step is rounded to dtype before the next
+            want = [torch.from_numpy(a).to(dtype).double().numpy() for a in want]
+        worst = 0.0
+        for s in range(n1 + n2):
+            err = O.rel_err(got[s], want[s])
+            worst = max(worst, err)
+        ok = worst <= max(TOL[dname], 0.0) if TOL[dname] else all(
+            np.array_equal(got[s], want[s]) for s in range(n1 + n2))
+        print(f"dist_check world={world} n1={n1} n2={n2} {dname} steps={steps} "
+              f"worst_rel_err={worst:.3e} {'PASS' if ok else 'FAIL'}", flush=True)
+    grp.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()

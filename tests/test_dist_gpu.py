@@ -1,0 +1,40 @@
+"""Multi-GPU sync over IPC peer memory (needs >= 2 GPUs; skipped otherwise)."""
+
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(n, *args):
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n),
+           os.path.join(ROOT, "scripts", "dist_check.py"), *map(str, args)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "PASS" in r.stdout
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "f64"])
+def test_two_gpus_tp4_tp3(dtype):
+    _run(2, 4, 3, dtype, 3)
+
+
+def test_two_gpus_tp2_tp1():
+    _run(2, 2, 1, "f32", 2)
+
+
+def test_four_gpus_tp2_tp1():
+    _run(4, 2, 1, "f32", 2)
+
+
+def test_eight_gpus_tp4_tp3():
+    _run(8, 4, 3, "bf16", 3)
