@@ -345,12 +345,13 @@ struct BulkSmem {
   uint64_t empty[kStages];
 };
 
-template <typename T, int OP, int kStages>
+template <typename T, int OP, int kStages, bool kSignaled>
 __global__ void __launch_bounds__(kBulkThreads, 1)
 plan_kernel_bulk(const Chunk *__restrict__ chunks, int n_chunks, BufTable bufs,
-                 typename Acc<T>::type wa, typename Acc<T>::type wb) {
+                 typename Acc<T>::type wa, typename Acc<T>::type wb, SignalArgs sig) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   auto &sm = *reinterpret_cast<BulkSmem<kStages> *>(smem_raw);
+  if (!cta_prologue<kSignaled>(sig)) return;
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   if (tid == 0) {
@@ -412,7 +413,20 @@ plan_kernel_bulk(const Chunk *__restrict__ chunks, int n_chunks, BufTable bufs,
     prev_stage = stage;
     if (++stage == kStages) { stage = 0; phase ^= 1u; }
   }
-  if (tid == 0) bulk_wait_all();
+  if (tid == 0) {
+    bulk_wait_all();  // this CTA's result stores are complete
+    if constexpr (kSignaled) {
+      // async-proxy (bulk) global writes -> generic release at system scope
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __threadfence_system();
+      const unsigned int done = atomicAdd(sig.counter, 1u);
+      if (done == gridDim.x - 1) {
+        __threadfence_system();
+        *sig.counter = 0u;
+        for (int i = 0; i < sig.n_post; ++i) st_release_sys(sig.post[i], sig.epoch);
+      }
+    }
+  }
 }
 
 template <typename T, int OP, bool kSignaled>
@@ -501,12 +515,13 @@ static int grid_for(K kernel, int device, int n_items) {
   return n_items < g ? (n_items > 0 ? n_items : 1) : g;
 }
 
-static std::atomic<int> g_sync_kernel{NTP_KERNEL_LDG};
+static std::atomic<int> g_sync_kernel{NTP_KERNEL_BULK};
 
-template <typename T, int OP, int kStages>
+template <typename T, int OP, int kStages, bool kSig>
 static int launch_bulk(const ntp_plan *p, const BufTable &bt, typename Acc<T>::type wa,
-                       typename Acc<T>::type wb, int ctas_per_sm, cudaStream_t s) {
-  auto k = plan_kernel_bulk<T, OP, kStages>;
+                       typename Acc<T>::type wb, int ctas_per_sm, const SignalArgs &sig,
+                       cudaStream_t s) {
+  auto k = plan_kernel_bulk<T, OP, kStages, kSig>;
   const int smem = (int)sizeof(BulkSmem<kStages>);
   static std::once_flag once[64];
   const int dev = p->device >= 0 && p->device < 64 ? p->device : 0;
@@ -516,7 +531,7 @@ static int launch_bulk(const ntp_plan *p, const BufTable &bt, typename Acc<T>::t
   const int n = (int)p->chunks.size();
   int grid = sm_count(p->device) * ctas_per_sm;
   if (n < grid) grid = n > 0 ? n : 1;
-  k<<<grid, kBulkThreads, smem, s>>>(p->d_chunks, n, bt, wa, wb);
+  k<<<grid, kBulkThreads, smem, s>>>(p->d_chunks, n, bt, wa, wb, sig);
   return NTP_OK;
 }
 
@@ -526,9 +541,10 @@ static int launch_plan_t(const ntp_plan *p, const BufTable &bt, double wa, doubl
   using A = typename Acc<T>::type;
   const int n = (int)p->chunks.size();
   const int variant = g_sync_kernel.load();
-  if (p->vectorized && !kSig && (variant == NTP_KERNEL_BULK || variant == NTP_KERNEL_BULK2)) {
-    if (variant == NTP_KERNEL_BULK) return launch_bulk<T, OP, 4>(p, bt, A(wa), A(wb), 1, s);
-    return launch_bulk<T, OP, 3>(p, bt, A(wa), A(wb), 2, s);
+  if (p->vectorized && (variant == NTP_KERNEL_BULK || variant == NTP_KERNEL_BULK2)) {
+    if (variant == NTP_KERNEL_BULK)
+      return launch_bulk<T, OP, 4, kSig>(p, bt, A(wa), A(wb), 1, sig, s);
+    return launch_bulk<T, OP, 3, kSig>(p, bt, A(wa), A(wb), 2, sig, s);
   }
   if (p->vectorized) {
     auto k = plan_kernel_vec<T, OP, kSig>;

@@ -225,7 +225,7 @@ def test_validation_messages(T):
     from paper_2504_06095_b200.shardmap import build_shard_map
     with pytest.raises(ValueError, match=r"replica degrees \(3, 4\) do not match map \(4, 3\)"):
         T.nonuniform_grad_sync(r, h, smap)
-    with pytest.raises(ValueError, match="map is over k=24 columns"):
+    with pytest.raises(ValueError, match="map is over k=25 columns, layer has ffn=24"):
         T.nonuniform_grad_sync(h, r, build_shard_map(25, 4, 3))
     with pytest.raises(ValueError, match="unknown reduction op 'max'"):
         T.nonuniform_grad_sync(h, r, smap, op="max")
@@ -290,7 +290,7 @@ def test_bulk_kernel_variants_match_oracle(T, variant):
             k = int(rng.integers(n1, 513))
             hidden = int(rng.choice([4, 8, 64, 1024]))
             for dtype in (torch.float32, torch.bfloat16):
-                _lib.check(L.ntp_set_option(0, 1))
+                _lib.check(L.ntp_set_option(0, 1))  # LDG reference variant
                 s1, h1, r1, hu, ru = make_case(T, k, n1, n2, hidden, i, dtype)
                 T.nonuniform_grad_sync(h1, r1, s1, weights=(0.25, 0.75))
                 _lib.check(L.ntp_set_option(0, variant))
@@ -302,4 +302,4 @@ def test_bulk_kernel_variants_match_oracle(T, variant):
                 check(h2, hb, dtype)
                 check(r2, rb, dtype)
     finally:
-        _lib.check(L.ntp_set_option(0, 1))
+        _lib.check(L.ntp_set_option(0, 2))
