@@ -199,7 +199,7 @@ def run_single(args):
     pk = peaks()
     hbm_bytes = 4 * S * eb  # read both replicas, write both
     achieved = hbm_bytes / (ms * 1e-3) / 1e9
-    roof = {"bound": "hbm", "kernel": "ntp::plan_kernel_vec<bf16,weighted>",
+    roof = {"bound": "hbm", "kernel": "ntp::plan_kernel_bulk<bf16,weighted,4>",
             "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "peak_src": pk["src"],
             "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
             "algorithmic_bytes_per_launch": hbm_bytes, "traffic": _ncu_traffic()}

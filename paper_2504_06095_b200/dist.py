@@ -5,17 +5,21 @@ replica's logical ranks are hosted by world ranks (processes, one GPU each);
 a process may host several logical ranks (e.g. N=2: the whole healthy
 replica on GPU 0, the reduced one on GPU 1).
 
-Data path (one-sided *push* from the reduced side):
+Data path (one-sided pulls + pushes over peer memory):
   * every logical rank's gradient arena is a cudaMalloc'd buffer exported with
-    CUDA IPC; each reduced-hosting process maps the healthy arenas it pairs
-    with (its sync shards' comp owners, shardmap.py:160-180);
-  * per step, healthy processes post a "ready" epoch into the reduced
-    processes' signal pages; each reduced process runs ONE kernel that waits
-    for its ready words, reads both copies of every unit of its sync shard (the
-    healthy copy over NVLink), reduces w_h*g_h + w_r*g_r in fp32, writes the
-    result to its own arena and into the healthy owner's arena (peer stores),
-    and finally posts "done" to the healthy processes;
-  * healthy processes block their stream on the done words.
+    CUDA IPC; each process maps the arenas of the processes it shares units
+    with (a reduced rank's sync shard pairs with its comp owners,
+    shardmap.py:160-180);
+  * every unit is computed by exactly one of its two owners' GPUs: for each
+    (healthy GPU, reduced GPU) pair the units are split in half, so both GPUs
+    read the partner's copy and write the result into both copies at once
+    (``unit_executors``); the busiest GPU's link bytes per direction stay at
+    the lower bound S_g*b;
+  * per step every process posts a "ready" epoch into its partners' signal
+    pages, runs ONE kernel that waits for its partners' ready words, reduces
+    w_h*g_h + w_r*g_r in fp32 for its units, writes both copies (local and peer
+    stores) and, once all its CTAs' stores have landed, posts "done"; the
+    stream then blocks on the partners' done words.
 This is the reference's pre-sync reshard + pairwise reduce + post-sync
 reshard (tpnumerics.py:323-356) as a single kernel with no staging buffer and
 no intermediate collective.  Regions whose layouts align (n1 == n2, or
@@ -76,13 +80,21 @@ class Placement:
         return self.h_proc[slot] if slot < self.n1 else self.r_proc[slot - self.n1]
 
 
-def process_plan_units(lay: PairLayout, plc: Placement, rank: int):
-    """The units `rank` computes (those whose reduced owner it hosts), as
-    per-segment (k, unit, cols, h_slot, h_off, r_slot, r_off) arrays in global
-    slot numbering, plus the set of peer slots it touches."""
+def unit_executors(lay: PairLayout, plc: Placement, policy: str = "split"):
+    """Per segment: (h_owner, h_off, r_owner, r_off, executor_proc) arrays over
+    the k units.  Units whose two owners share a process run there.  Otherwise
+    ``policy`` decides which endpoint computes the unit:
+
+    * "split" (default): for every (healthy proc, reduced proc) pair, the first
+      half of the pair's units (in column order) run on the reduced side and
+      the second half on the healthy side -- both GPUs read and write over the
+      link at once (measured: ~700 GB/s per direction vs ~495 GB/s when one
+      side both reads and writes everything, profiles/r01_nvlink_probe.json);
+    * "reduced": every unit runs on its reduced owner's GPU (pure push).
+    """
     out = []
-    touched = set()
-    my_red = {j for j, p in enumerate(plc.r_proc) if p == rank}
+    hp_of = np.asarray(plc.h_proc)
+    rp_of = np.asarray(plc.r_proc)
     for k, unit, hc, rc, hb, rb in lay.segs:
         h_owner = np.empty(k, dtype=np.int64)
         h_off = np.empty(k, dtype=np.int64)
@@ -94,7 +106,26 @@ def process_plan_units(lay: PairLayout, plc: Placement, rank: int):
         for r, c in enumerate(rc):
             r_owner[c] = r
             r_off[c] = rb[r] + np.arange(len(c)) * unit
-        sel = np.flatnonzero(np.isin(r_owner, list(my_red)))
+        hp, rp = hp_of[h_owner], rp_of[r_owner]
+        ex = rp.copy()
+        if policy == "split":
+            key = hp * (1 << 20) + rp
+            for kv in np.unique(key[hp != rp]):
+                idx = np.flatnonzero(key == kv)
+                ex[idx[(len(idx) + 1) // 2:]] = hp[idx[0]]
+        elif policy != "reduced":
+            raise ValueError(f"unknown executor policy {policy!r}")
+        out.append((unit, h_owner, h_off, r_owner, r_off, ex))
+    return out
+
+
+def process_plan_units(lay: PairLayout, plc: Placement, rank: int, policy: str = "split"):
+    """The units `rank` computes, as per-segment (unit, h_slot, h_off, r_slot,
+    r_off) arrays in global slot numbering, plus the set of slots it touches."""
+    out = []
+    touched = set()
+    for unit, h_owner, h_off, r_owner, r_off, ex in unit_executors(lay, plc, policy):
+        sel = np.flatnonzero(ex == rank)
         if len(sel) == 0:
             continue
         out.append((unit, h_owner[sel], h_off[sel], plc.n1 + r_owner[sel], r_off[sel]))
@@ -118,15 +149,14 @@ def exchange_pairs(lay: PairLayout, plc: Placement) -> set:
     return pairs
 
 
-def signal_wiring(lay: PairLayout, plc: Placement, rank: int):
-    """(ready_from, done_to, done_from): world ranks this process waits on for
-    'ready', posts 'done' to (as a reduced host), and waits on for 'done' (as a
-    healthy host).  Same-process pairs need no signal."""
+def partners(lay: PairLayout, plc: Placement, rank: int) -> list:
+    """World ranks this process exchanges units with (either direction).  Every
+    step, a process posts "ready" to each partner, runs its kernel (which waits
+    for the partners' "ready" and posts "done" to them when all its stores have
+    landed) and then waits for each partner's "done"."""
     pairs = exchange_pairs(lay, plc)
-    ready_from = sorted({h for h, r in pairs if r == rank and h != rank})
-    done_to = ready_from
-    done_from = sorted({r for h, r in pairs if h == rank and r != rank})
-    return ready_from, done_to, done_from
+    return sorted({r for h, r in pairs if h == rank and r != rank} |
+                  {h for h, r in pairs if r == rank and h != rank})
 
 
 class DeviceOps:
@@ -175,8 +205,8 @@ class NtpSyncGroup:
     """One process's share of a distributed nonuniform gradient sync."""
 
     def __init__(self, lay: PairLayout, placement: Placement, dtype: torch.dtype, device: int,
-                 ops: DeviceOps | None = None, group=None):
-        self.lay, self.plc, self.dtype = lay, placement, dtype
+                 ops: DeviceOps | None = None, group=None, policy: str = "split"):
+        self.lay, self.plc, self.dtype, self.policy = lay, placement, dtype, policy
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.device = device
@@ -195,17 +225,15 @@ class NtpSyncGroup:
         dist.all_gather_object(table, mine, group=group)
         self.table = table
         # 3. what this process computes, and which peer buffers it needs
-        units, touched = process_plan_units(lay, placement, self.rank)
-        self.ready_from, self.done_to, self.done_from = signal_wiring(lay, placement, self.rank)
+        units, touched = process_plan_units(lay, placement, self.rank, policy)
+        self.partners = partners(lay, placement, self.rank)
         self.opened = {}
         self.slot_ptr = dict(self.local)
         for s in sorted(touched):
             if s not in self.slot_ptr:
                 proc = placement.proc_of_slot(s)
                 self.slot_ptr[s] = self.opened[s] = self.ops.open(table[proc]["slots"][s])
-        self.peer_sig = {}
-        for p in set(self.done_to) | set(self.done_from) | set(self.ready_from):
-            self.peer_sig[p] = self.ops.open(table[p]["sig"])
+        self.peer_sig = {p: self.ops.open(table[p]["sig"]) for p in self.partners}
         # 4. the plan, with buffers renumbered to a dense local table
         order = sorted(self.slot_ptr)
         self.buf_index = {s: i for i, s in enumerate(order)}
@@ -220,12 +248,13 @@ class NtpSyncGroup:
                 plan.add_units(unit, remap[hs], ho, remap[rs], ro)
             self.plan = plan.finalize()
         self.units = sum(len(u[1]) for u in units)
-        # signal words: where I wait / where I post
-        self.wait_ready = [self.sig + 8 * (READY * SIG_WORDS + p) for p in self.ready_from]
-        self.post_done = [self.peer_sig[p] + 8 * (DONE * SIG_WORDS + self.rank) for p in self.done_to]
+        # signal words (slot = writer's world rank in the receiver's page)
         self.post_ready = [self.peer_sig[p] + 8 * (READY * SIG_WORDS + self.rank)
-                           for p in self.done_from]
-        self.wait_done = [self.sig + 8 * (DONE * SIG_WORDS + p) for p in self.done_from]
+                           for p in self.partners]
+        self.wait_ready = [self.sig + 8 * (READY * SIG_WORDS + p) for p in self.partners]
+        self.post_done = [self.peer_sig[p] + 8 * (DONE * SIG_WORDS + self.rank)
+                          for p in self.partners]
+        self.wait_done = [self.sig + 8 * (DONE * SIG_WORDS + p) for p in self.partners]
         self.epoch = 0
         self._status = None
 
@@ -253,12 +282,18 @@ class NtpSyncGroup:
             _lib.check(L.ntp_signal_post(_lib.u64_ptr_array(self.post_ready), len(self.post_ready),
                                          e, sp), "ntp_signal_post")
         if self.plan is not None:
-            if self.wait_ready or self.post_done:
+            if self.partners:
                 self.plan.grad_sync_signaled(self.bufs, OPS["weighted"], w_h, w_r,
                                              self.wait_ready, self.post_done, e, spin_ns,
                                              self._status.data_ptr(), s)
             else:
                 self.plan.grad_sync(self.bufs, OPS["weighted"], w_h, w_r, s)
+        elif self.partners:
+            # nothing to compute: wait until partners may be touched, then release them
+            _lib.check(L.ntp_signal_wait(_lib.u64_ptr_array(self.wait_ready), len(self.wait_ready),
+                                         e, spin_ns, st, sp), "ntp_signal_wait")
+            _lib.check(L.ntp_signal_post(_lib.u64_ptr_array(self.post_done), len(self.post_done),
+                                         e, sp), "ntp_signal_post")
         if self.wait_done:
             _lib.check(L.ntp_signal_wait(_lib.u64_ptr_array(self.wait_done), len(self.wait_done),
                                          e, spin_ns, st, sp), "ntp_signal_wait")

@@ -92,7 +92,7 @@ def run(args):
                           "busiest_gpu_bytes_per_direction": B,
                           "weights": [round(W_H, 6), round(W_R, 6)],
                           "l2": "inputs >> L2"},
-               "roofline": {"bound": "nvlink", "kernel": "ntp::plan_kernel_vec<bf16,weighted,signaled>",
+               "roofline": {"bound": "nvlink", "kernel": "ntp::plan_kernel_bulk<bf16,weighted,4,signaled>",
                             "achieved": round(achieved, 1), "peak": pk["nvlink_gbs"],
                             "peak_src": "measured peer copy 770 GB/s/direction (B200_PROFILING.md)",
                             "unit": "GB/s", "frac": round(achieved / pk["nvlink_gbs"], 4),

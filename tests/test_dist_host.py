@@ -61,7 +61,7 @@ def _worker(rank, world, port, n1, n2, q):
     tab = g.plan.export() if g.plan is not None else np.zeros((0, 5), dtype=np.int64)
     slots = sorted(g.slot_ptr)
     q.put((rank, tab, slots, g.wait_ready, g.post_done, g.post_ready, g.wait_done,
-           g.ready_from, g.done_to, g.done_from, g.sig))
+           g.partners, g.sig))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -116,17 +116,16 @@ def _replay(lay, per_rank, w=(4 / 7, 3 / 7), seed=0):
 
 
 def _check_wiring(per_rank):
-    ready_posts = set()
-    ready_waits = set()
-    done_posts = set()
-    done_waits = set()
-    for rank, (_t, _s, _wr, _pd, _pr, _wd, ready_from, done_to, done_from, _sig) in per_rank.items():
-        ready_waits |= {(p, rank) for p in ready_from}
-        done_posts |= {(rank, p) for p in done_to}
-        ready_posts |= {(rank, p) for p in done_from}   # healthy posts ready to its reduced peers
-        done_waits |= {(p, rank) for p in done_from}
-    assert ready_posts == ready_waits
-    assert done_posts == done_waits
+    """Partner sets are symmetric; every posted word is a word its owner waits on."""
+    sig_base = {rank: v[-1] for rank, v in per_rank.items()}
+    for rank, (_t, _s, wr, pd, pr, wd, partners, sig) in per_rank.items():
+        for p in partners:
+            assert rank in per_rank[p][6]
+        # my posts land in the partner's page at slot = my rank
+        assert sorted(pr) == sorted(sig_base[p] + 8 * (D.READY * D.SIG_WORDS + rank) for p in partners)
+        assert sorted(pd) == sorted(sig_base[p] + 8 * (D.DONE * D.SIG_WORDS + rank) for p in partners)
+        assert sorted(wr) == sorted(sig + 8 * (D.READY * D.SIG_WORDS + p) for p in partners)
+        assert sorted(wd) == sorted(sig + 8 * (D.DONE * D.SIG_WORDS + p) for p in partners)
 
 
 @pytest.mark.parametrize("n1,n2", [(4, 3), (2, 1)])
@@ -135,8 +134,20 @@ def test_gloo_world2_plans_and_wiring(n1, n2):
     lay = pair_layout(SHAPE, n1, n2)
     _replay(lay, per_rank)
     _check_wiring(per_rank)
-    # world 2: healthy replica on rank 0, reduced on rank 1; rank 1 does all the work
-    assert len(per_rank[0][0]) == 0 and len(per_rank[1][0]) > 0
+    # world 2, split policy: both GPUs push about half of the shared units
+    e0 = per_rank[0][0][:, 4].sum()
+    e1 = per_rank[1][0][:, 4].sum()
+    assert abs(int(e0) - int(e1)) <= 0.1 * (e0 + e1)
+
+
+def test_reduced_policy_pushes_from_reduced_side():
+    lay = pair_layout(SHAPE, 4, 3)
+    plc = D.Placement.default(2, 4, 3)
+    u0, _ = D.process_plan_units(lay, plc, 0, policy="reduced")
+    u1, _ = D.process_plan_units(lay, plc, 1, policy="reduced")
+    assert u0 == [] and len(u1) > 0
+    with pytest.raises(ValueError):
+        D.unit_executors(lay, plc, policy="other")
 
 
 def test_placements():
