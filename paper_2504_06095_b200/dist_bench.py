@@ -30,6 +30,7 @@ def _max(x: float) -> float:
 def run(args):
     from bench import METRIC, W_H, W_R, ClockSampler, peaks  # noqa: I001 (repo root on sys.path)
 
+    os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if not dist.is_initialized():
@@ -102,6 +103,8 @@ def run(args):
                "clocks": clk, "e2e": e2e}
     dist.barrier()
     grp.close()
+    dist.barrier()
+    dist.destroy_process_group()
     return out
 
 
