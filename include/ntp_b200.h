@@ -167,6 +167,28 @@ int ntp_uniform_sync(void *const *reps, int R, int64_t n, int dtype, int op, con
                      void *stream);
 
 /* ------------------------------------------------------------------------
+ * Uneven-shard linears on tcgen05 tensor cores (bf16 in, fp32 accumulate)
+ * ------------------------------------------------------------------------ */
+
+enum ntp_gemm_epilogue {
+  NTP_EPI_NONE = 0,  /* C = alpha * acc                                            */
+  NTP_EPI_GELU = 1,  /* aux = bf16(alpha*acc) (pre-activation H); C = GeLU(aux)    */
+  NTP_EPI_DGELU = 2  /* C = alpha * acc * GeLU'(aux)   (aux = H, backward)         */
+};
+
+/* C[M x N] = epilogue(sum_k A[m,k] * B[n,k]) -- the per-rank GEMMs of
+ * mlp_forward_tp / mlp_backward_tp (tpnumerics.py:177-185, 238-252) with
+ * ragged M/N/K (n_i = 4779, 1366, ...).  A is [M x K]: a_mn = 0 -> stored
+ * row-major [M][lda] (K contiguous), a_mn = 1 -> stored [K][lda] (M
+ * contiguous).  B likewise for [N x K] with b_mn.  C is row-major [M][ldc]
+ * (bf16, or fp32 if c_f32); ldc may exceed N, e.g. 2*hidden to write the
+ * unit-major gradient arena directly.  A, B, aux: bf16, 16-byte aligned
+ * bases and row pitches.  Stream-ordered. */
+int ntp_gemm_bf16(const void *A, int64_t lda, int a_mn, const void *B, int64_t ldb, int b_mn,
+                  void *C, int64_t ldc, int c_f32, int64_t M, int64_t N, int64_t K, int epilogue,
+                  const void *aux, int64_t ld_aux, float alpha, void *stream);
+
+/* ------------------------------------------------------------------------
  * Multi-GPU plumbing: peer memory over NVLink/NVSwitch and device signals
  * ------------------------------------------------------------------------ */
 

@@ -64,6 +64,10 @@ SIGNATURES = {
     "ntp_reshard": (ctypes.c_int, [_vp, _vpp, ctypes.c_int, _vp]),
     "ntp_uniform_sync": (ctypes.c_int, [_vpp, ctypes.c_int, ctypes.c_int64, ctypes.c_int,
                                         ctypes.c_int, ctypes.POINTER(ctypes.c_double), _vp]),
+    "ntp_gemm_bf16": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int, _vp, ctypes.c_int64,
+                                     ctypes.c_int, _vp, ctypes.c_int64, ctypes.c_int,
+                                     ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                     _vp, ctypes.c_int64, ctypes.c_float, _vp]),
     "ntp_alloc": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, _vpp]),
     "ntp_free": (ctypes.c_int, [_vp]),
     "ntp_ipc_get_handle": (ctypes.c_int, [_vp, ctypes.c_char_p]),

@@ -1,0 +1,136 @@
+"""Uneven-shard column/row-parallel MLP linears on tcgen05 (``ntp_gemm_bf16``).
+
+Per TP rank i the reference computes (tpnumerics.py:177-185, 238-252)
+
+    H_i = X A_i        Y_i = GeLU(H_i)        Z = sum_i Y_i B_i
+    dB_i = Y_i^T G     D_i = (G B_i^T) * GeLU'(H_i)     dA_i = X^T D_i
+
+with ragged n_i columns per rank (shardmap.py:160-165).  Here every rank's
+weights are stored **unit-major**, exactly like its gradients: ``W[p, 0, :]`` is
+column p of A_i and ``W[p, 1, :]`` is row p of B_i.  All five GEMMs read that
+layout in place (K-major or MN-major TMA views with a 2*hidden row pitch), and
+the two weight-gradient GEMMs write ``grads[p, 0, :]`` / ``grads[p, 1, :]``
+directly -- the arena the sync kernel consumes, with no repacking.
+
+Numerics: bf16 operands, fp32 accumulation in TMEM; H, Y and D are kept in
+bf16, Z in fp32 (the TP partial sums).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+
+EPI = {"none": 0, "gelu": 1, "dgelu": 2}
+
+
+def _operand(t: torch.Tensor):
+    """(ptr, ld, mn_major) of a logical [rows x K] bf16 view."""
+    if t.dtype != torch.bfloat16:
+        raise ValueError("tcgen05 GEMM operands are bf16")
+    if t.dim() != 2:
+        raise ValueError("GEMM operands are 2-D views")
+    if t.stride(1) == 1:
+        return t.data_ptr(), t.stride(0), 0
+    if t.stride(0) == 1:
+        return t.data_ptr(), t.stride(1), 1
+    raise ValueError("GEMM operand must have a unit stride in one dimension")
+
+
+def mm(A: torch.Tensor, Bt: torch.Tensor, out: torch.Tensor, *, epilogue: str = "none",
+       aux: torch.Tensor | None = None, alpha: float = 1.0, stream=None) -> torch.Tensor:
+    """out[M x N] = epilogue(A[M x K] @ Bt[N x K]^T) on the tensor cores.
+
+    A and Bt may be K-major or MN-major views (e.g. ``Y.T``); ``out`` is a
+    row-major [M x N] view with any row pitch (bf16 or fp32)."""
+    M, K = A.shape
+    N, K2 = Bt.shape
+    if K != K2 or tuple(out.shape) != (M, N):
+        raise ValueError(f"shape mismatch: A {tuple(A.shape)}, Bt {tuple(Bt.shape)}, out {tuple(out.shape)}")
+    if out.stride(1) != 1:
+        raise ValueError("out must be row-major")
+    if out.dtype not in (torch.bfloat16, torch.float32):
+        raise ValueError("out must be bf16 or fp32")
+    a_ptr, lda, a_mn = _operand(A)
+    b_ptr, ldb, b_mn = _operand(Bt)
+    aux_ptr, ld_aux = (0, 0)
+    if epilogue != "none":
+        if aux is None or aux.dtype != torch.bfloat16 or tuple(aux.shape) != (M, N) or aux.stride(1) != 1:
+            raise ValueError("epilogue needs a bf16 row-major aux [M x N]")
+        aux_ptr, ld_aux = aux.data_ptr(), aux.stride(0)
+    if stream is None:
+        stream = torch.cuda.current_stream(A.device)
+    _lib.check(_lib.load().ntp_gemm_bf16(
+        ctypes.c_void_p(a_ptr), lda, a_mn, ctypes.c_void_p(b_ptr), ldb, b_mn,
+        ctypes.c_void_p(out.data_ptr()), out.stride(0), int(out.dtype == torch.float32),
+        M, N, K, EPI[epilogue], ctypes.c_void_p(aux_ptr), ld_aux, float(alpha),
+        ctypes.c_void_p(stream.cuda_stream)), "ntp_gemm_bf16")
+    return out
+
+
+def _pad8(n: int) -> int:
+    return (n + 7) // 8 * 8
+
+
+class MlpShard:
+    """One TP rank's slice of an MLP block: unit-major bf16 weights [n, 2, h]."""
+
+    def __init__(self, A: np.ndarray, B: np.ndarray, cols, device="cuda"):
+        cols = np.asarray(cols, dtype=np.int64)
+        h = A.shape[0]
+        w = np.empty((len(cols), 2, h))
+        w[:, 0, :] = A[:, cols].T
+        w[:, 1, :] = B[cols, :]
+        self.n, self.h = len(cols), h
+        self.W = torch.from_numpy(w).to(device=device, dtype=torch.bfloat16)
+        self.H = self.Y = None
+
+    def forward(self, X: torch.Tensor, Z: torch.Tensor, accumulate: bool = False) -> None:
+        """H = X A_i, Y = GeLU(H) (fused epilogue), Z (+)= Y B_i (fp32 partial)."""
+        T = X.shape[0]
+        npad = _pad8(self.n)
+        if self.H is None or self.H.shape[0] != T:
+            self.H = torch.empty((T, npad), dtype=torch.bfloat16, device=X.device)
+            self.Y = torch.empty((T, npad), dtype=torch.bfloat16, device=X.device)
+        H, Y = self.H[:, :self.n], self.Y[:, :self.n]
+        mm(X, self.W[:, 0, :], Y, epilogue="gelu", aux=H)
+        if accumulate:
+            part = torch.empty((T, self.h), dtype=torch.float32, device=X.device)
+            mm(Y, self.W[:, 1, :].T, part)
+            Z += part
+        else:
+            mm(Y, self.W[:, 1, :].T, Z)
+
+    def backward(self, X: torch.Tensor, G: torch.Tensor, grads: torch.Tensor) -> None:
+        """Weight gradients written unit-major into grads [n, 2, h] (bf16 or fp32):
+        grads[:, 1, :] = Y^T G, grads[:, 0, :] = D^T X with D = (G B_i^T) * GeLU'(H)."""
+        T = X.shape[0]
+        H, Y = self.H[:, :self.n], self.Y[:, :self.n]
+        Dfull = torch.empty((T, _pad8(self.n)), dtype=torch.bfloat16, device=X.device)
+        D = Dfull[:, :self.n]
+        mm(G, self.W[:, 1, :], D, epilogue="dgelu", aux=H)
+        mm(Y.T, G.T, grads[:, 1, :])
+        mm(D.T, X.T, grads[:, 0, :])
+
+
+def mlp_forward_tp(X: torch.Tensor, shards) -> torch.Tensor:
+    """Z = sum_i GeLU(X A_i) B_i in ascending rank order (tpnumerics.py:177-185);
+    on one GPU the TP all-reduce is this ordered sum."""
+    Z = torch.zeros((X.shape[0], shards[0].h), dtype=torch.float32, device=X.device)
+    for i, sh in enumerate(shards):
+        sh.forward(X, Z, accumulate=i > 0)
+    return Z
+
+
+def mlp_backward_tp(X: torch.Tensor, shards, G: torch.Tensor, replica) -> None:
+    """Parameter gradients of every rank straight into ``replica.grads`` (the
+    unit-major arenas of a tpnumerics.MlpReplica built on the same columns)."""
+    for sh, g in zip(shards, replica.grads):
+        if tuple(g.shape) != (sh.n, 2, sh.h):
+            raise ValueError("replica layout does not match the shards")
+        sh.backward(X, G, g)
+    replica._has_grads = True

@@ -1,0 +1,140 @@
+"""tcgen05 uneven-shard linears (ntp_gemm_bf16 / paper_2504_06095_b200.linear).
+
+Floating-point kernel: each GEMM is checked against a plain torch fp32
+evaluation of the same bf16 operands; the TP MLP chain against the oracle's
+fp64 restatement of the reference (mlp_backward_tp, tpnumerics.py:238-252)
+with the bf16 tolerance of the north_star (2e-2 Frobenius)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def Lin():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2504_06095_b200 import linear
+    return linear
+
+
+def rel(a, b):
+    a, b = a.double(), b.double()
+    return ((a - b).norm() / b.norm().clamp_min(1e-30)).item()
+
+
+def _mk(rows, cols, mn, g):
+    """A logical [rows x cols] bf16 view that is K-major (mn=0) or MN-major (mn=1)."""
+    if mn:
+        return torch.randn((cols, rows), generator=g, device="cuda").to(torch.bfloat16).T
+    return torch.randn((rows, cols), generator=g, device="cuda").to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 256), (300, 4779, 200),
+                                   (1366, 1024, 1000), (1, 8, 8), (130, 136, 72)])
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def test_gemm_all_layouts(Lin, M, N, K, a_mn, b_mn):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N * 3 + K + a_mn * 2 + b_mn)
+    if a_mn and M % 8:
+        pytest.skip("MN-major needs a 16-byte row pitch")
+    if b_mn and N % 8:
+        pytest.skip("MN-major needs a 16-byte row pitch")
+    if not a_mn and K % 8 or not b_mn and K % 8:
+        pytest.skip("K-major needs a 16-byte row pitch")
+    A = _mk(M, K, a_mn, g)
+    B = _mk(N, K, b_mn, g)
+    want = A.float() @ B.float().T
+    out = torch.empty((M, N), dtype=torch.float32, device="cuda")
+    Lin.mm(A, B, out)
+    torch.cuda.synchronize()
+    assert rel(out, want) < 1e-5
+    outb = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+    Lin.mm(A, B, outb, alpha=0.5)
+    assert rel(outb.float(), 0.5 * want) < 5e-3
+
+
+def test_gemm_epilogues_and_pitch(Lin):
+    g = torch.Generator(device="cuda").manual_seed(5)
+    M, N, K = 512, 4779, 256
+    A = _mk(M, K, 0, g)
+    B = _mk(N, K, 0, g)
+    acc = A.float() @ B.float().T
+    npad = (N + 7) // 8 * 8
+    H = torch.empty((M, npad), dtype=torch.bfloat16, device="cuda")[:, :N]
+    Y = torch.empty((M, npad), dtype=torch.bfloat16, device="cuda")[:, :N]
+    Lin.mm(A, B, Y, epilogue="gelu", aux=H)
+    assert rel(H.float(), acc) < 5e-3
+    want = O.gelu(H.double().cpu().numpy())
+    assert rel(Y.float().cpu(), torch.from_numpy(want)) < 5e-3
+    D = torch.empty((M, npad), dtype=torch.bfloat16, device="cuda")[:, :N]
+    Lin.mm(A, B, D, epilogue="dgelu", aux=H)
+    want = acc.double().cpu().numpy() * O.gelu_grad(H.double().cpu().numpy())
+    assert rel(D.float().cpu(), torch.from_numpy(want)) < 5e-3
+    # output row pitch 2*N into an interleaved arena (the unit-major gradient layout)
+    arena = torch.zeros((M, 2, N), dtype=torch.float32, device="cuda")
+    Lin.mm(A, B, arena[:, 1, :])
+    assert rel(arena[:, 1, :], acc) < 1e-5 and arena[:, 0, :].abs().max().item() == 0.0
+
+
+def test_tp_mlp_forward_backward_vs_oracle(Lin):
+    """TP4 comp layout of (1000, 4, 3): ragged, non-contiguous shards."""
+    from paper_2504_06095_b200 import tpnumerics as T
+    from paper_2504_06095_b200.shardmap import build_shard_map
+    h, k, tok = 256, 1000, 512
+    A, B = O.random_layer(h, k, seed=1)
+    A, B = A / np.sqrt(h), B / np.sqrt(k)
+    smap = build_shard_map(k, 4, 3)
+    rng = np.random.default_rng(2)
+    X = rng.standard_normal((tok, h))
+    G = rng.standard_normal((tok, h))
+    bf = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(torch.bfloat16)  # noqa: E731
+    r64 = lambda x: bf(x).double().numpy()  # noqa: E731
+    A, B, X, G = r64(A), r64(B), r64(X), r64(G)
+    for cols in (T.assignment_from_comp(smap), T.assignment_from_sync(smap)):
+        shards = [Lin.MlpShard(A, B, c) for c in cols]
+        Xd, Gd = bf(X).cuda(), bf(G).cuda()
+        Z = Lin.mlp_forward_tp(Xd, shards)
+        Zref = O.mlp_forward_dense(X, A, B)
+        assert rel(Z.cpu(), torch.from_numpy(Zref)) < 2e-2
+        rep = T.MlpReplica(T.MlpLayer(A, B), cols, dtype=torch.float32)
+        Lin.mlp_backward_tp(Xd, shards, Gd, rep)
+        want = O.mlp_backward_tp(X, A, B, G, cols)
+        for u, (ga, gb) in zip(rep.units(), want):
+            got_a, got_b = O.from_units(u, h)
+            assert rel(torch.from_numpy(got_a), torch.from_numpy(ga)) < 2e-2
+            assert rel(torch.from_numpy(got_b), torch.from_numpy(gb)) < 2e-2
+
+
+def test_tensor_core_grads_then_sync(Lin):
+    """Producer -> sync chain: tcgen05 wgrad writes the unit-major arenas that
+    nonuniform_grad_sync reduces; the result matches the dense fp64 sum."""
+    from paper_2504_06095_b200 import tpnumerics as T
+    from paper_2504_06095_b200.shardmap import build_shard_map
+    h, k, tok = 128, 600, 256
+    A, B = O.random_layer(h, k, seed=3)
+    A, B = A / np.sqrt(h), B / np.sqrt(k)
+    smap = build_shard_map(k, 4, 3)
+    rng = np.random.default_rng(4)
+    bf = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(torch.bfloat16)  # noqa: E731
+    r64 = lambda x: bf(x).double().numpy()  # noqa: E731
+    A, B = r64(A), r64(B)
+    X1, G1, X2, G2 = (r64(rng.standard_normal((tok, h))) for _ in range(4))
+    layer = T.MlpLayer(A, B)
+    reps = []
+    for cols, X, G in ((T.assignment_from_comp(smap), X1, G1), (T.assignment_from_sync(smap), X2, G2)):
+        shards = [Lin.MlpShard(A, B, c) for c in cols]
+        rep = T.MlpReplica(layer, cols, dtype=torch.bfloat16)
+        Lin.mlp_forward_tp(bf(X).cuda(), shards)
+        Lin.mlp_backward_tp(bf(X).cuda(), shards, bf(G).cuda(), rep)
+        reps.append(rep)
+    T.nonuniform_grad_sync(reps[0], reps[1], smap)
+    da1, db1 = O.mlp_backward(X1, A, B, G1)
+    da2, db2 = O.mlp_backward(X2, A, B, G2)
+    for rep in reps:
+        da, db = rep.dense_grads()
+        assert O.rel_err(da, da1 + da2) < 2e-2
+        assert O.rel_err(db, db1 + db2) < 2e-2
