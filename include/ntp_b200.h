@@ -167,6 +167,28 @@ int ntp_uniform_sync(void *const *reps, int R, int64_t n, int dtype, int op, con
                      void *stream);
 
 /* ------------------------------------------------------------------------
+ * R-way sync for DP > 2 (no reference function: composes nonuniform_grad_sync,
+ * tpnumerics.py:289-356, with uniform_grad_sync, 263-286)
+ * ------------------------------------------------------------------------ */
+
+typedef struct ntp_mplan ntp_mplan;
+
+/* R in [2, 8] replicas; dtype NTP_BF16 or NTP_F32. */
+int ntp_mplan_create(ntp_mplan **out, int dtype, int R);
+/* bufs/offs are [R][n_units] (replica-major): unit j of replica r lives at
+ * bufs[bufs[r*n_units+j]] + offs[r*n_units+j] (elements). */
+int ntp_mplan_add_units(ntp_mplan *plan, int64_t n_units, int64_t unit_elems, const int32_t *bufs,
+                        const int64_t *offs);
+int ntp_mplan_finalize(ntp_mplan *plan);
+int64_t ntp_mplan_chunks(const ntp_mplan *plan);
+int ntp_mplan_upload(ntp_mplan *plan, int device);
+void ntp_mplan_destroy(ntp_mplan *plan);
+/* Every unit ends as op over its R copies (SUM in replica order, true MEAN, or
+ * sum_r w[r]*x_r), written to all R owners; one read and one write per copy. */
+int ntp_multi_sync(const ntp_mplan *plan, void *const *bufs, int n_bufs, int op, const double *w,
+                   void *stream);
+
+/* ------------------------------------------------------------------------
  * Uneven-shard linears on tcgen05 tensor cores (bf16 in, fp32 accumulate)
  * ------------------------------------------------------------------------ */
 

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libntp_b200.so")
 
-SOURCES = ["ntp_planner.cpp", "ntp_sync.cu", "ntp_linear.cu"]
+SOURCES = ["ntp_planner.cpp", "ntp_sync.cu", "ntp_linear.cu", "ntp_multi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

@@ -130,3 +130,55 @@ def _stream_ptr(stream, device):
 
 def tensor_ptrs(tensors) -> list[int]:
     return [int(t.data_ptr()) for t in tensors]
+
+
+class MultiPlan:
+    """Owns an ``ntp_mplan``: R-way unit tables for DP > 2 syncs."""
+
+    def __init__(self, dtype: int, R: int):
+        self._L = _lib.load()
+        h = ctypes.c_void_p()
+        _lib.check(self._L.ntp_mplan_create(ctypes.byref(h), int(dtype), int(R)), "ntp_mplan_create")
+        self._h, self.dtype, self.R, self.device = h, int(dtype), int(R), None
+
+    def add_units(self, unit_elems: int, bufs, offs) -> "MultiPlan":
+        """bufs, offs: [R x n_units] arrays (replica-major)."""
+        b = np.ascontiguousarray(bufs, dtype=np.int32)
+        o = np.ascontiguousarray(offs, dtype=np.int64)
+        if b.shape != o.shape or b.ndim != 2 or b.shape[0] != self.R:
+            raise ValueError("bufs/offs must be [R x n_units]")
+        _lib.check(self._L.ntp_mplan_add_units(self._h, b.shape[1], int(unit_elems), _lib.p32(b),
+                                               _lib.p64(o)), "ntp_mplan_add_units")
+        return self
+
+    def finalize(self) -> "MultiPlan":
+        _lib.check(self._L.ntp_mplan_finalize(self._h), "ntp_mplan_finalize")
+        return self
+
+    @property
+    def n_chunks(self) -> int:
+        return _lib.check(self._L.ntp_mplan_chunks(self._h))
+
+    def upload(self, device: int) -> "MultiPlan":
+        _lib.check(self._L.ntp_mplan_upload(self._h, int(device)), "ntp_mplan_upload")
+        self.device = int(device)
+        return self
+
+    def sync(self, bufs, op: int, weights=None, stream=None) -> None:
+        w = None
+        if weights is not None:
+            w = np.ascontiguousarray(weights, dtype=np.float64)
+            if len(w) != self.R:
+                raise ValueError("one weight per replica")
+            w = w.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        _lib.check(self._L.ntp_multi_sync(self._h, _lib.ptr_array(bufs), len(bufs), int(op), w,
+                                          _stream_ptr(stream, self.device)), "ntp_multi_sync")
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                self._L.ntp_mplan_destroy(h)
+            except Exception:
+                pass
+            self._h = None

@@ -325,3 +325,41 @@ def uniform_grad_sync(replicas, op: str = "sum", weights=None) -> None:
                                       dtype_code(first.dtype), code, wp,
                                       ctypes.c_void_p(stream.cuda_stream)),
                    "ntp_uniform_sync")
+
+
+def multi_grad_sync(replicas, op: str = "sum", weights=None) -> None:
+    """DP > 2 sync across replicas of ANY layouts (healthy TP-n and degraded
+    TP-m mixed), in place: every unit ends as the reduction of its R copies in
+    replica order -- uniform_grad_sync's "sum"/"mean" semantics
+    (tpnumerics.py:263-286) over nonuniform_grad_sync's layouts (289-356), or
+    the batch-weighted sum with ``weights`` (one per replica).  One kernel reads
+    each copy once and writes the result into every owner."""
+    from .plans import MultiPlan
+    first = replicas[0]
+    if len(replicas) < 2:
+        raise ValueError("need at least two replicas")
+    for rep in replicas:
+        if rep.grad_a is None:
+            raise ValueError("replica holds no gradients")
+        if rep.layer.ffn != first.layer.ffn or rep.hidden != first.hidden:
+            raise ValueError("replicas hold different layers")
+        if not isinstance(rep, MlpReplica) or rep.dtype != first.dtype or rep.device != first.device:
+            raise ValueError("replicas must be device MlpReplicas of one dtype and device")
+    if op not in ("sum", "mean"):
+        raise ValueError(f"unknown reduction op {op!r}")
+    code = OPS[op]
+    if weights is not None:
+        if op != "sum" or len(weights) != len(replicas):
+            raise ValueError("weights= needs op='sum' and one weight per replica")
+        code = OPS["weighted"]
+    k, unit = first.layer.ffn, 2 * first.hidden
+    bufs, offs, base = [], [], 0
+    for rep in replicas:
+        owner, off = layout_offsets(rep.cols, k, unit)
+        bufs.append(owner + base)
+        offs.append(off)
+        base += rep.n
+    dev = first.device.index if first.device.index is not None else torch.cuda.current_device()
+    plan = MultiPlan(dtype_code(first.dtype), len(replicas)).add_units(unit, bufs, offs)
+    plan.finalize().upload(dev)
+    plan.sync(tensor_ptrs([g for rep in replicas for g in rep.grads]), code, weights)
