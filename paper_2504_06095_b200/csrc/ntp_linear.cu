@@ -132,53 +132,75 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
 struct Params {
   int M, N, K;
   int a_mn, b_mn;          // 1 = operand is MN-major in global memory
-  void *C;
-  long long ldc;           // elements
   int c_f32;               // 1: fp32 output, 0: bf16
   int epi;
-  const __nv_bfloat16 *aux;  // EPI_DGELU: H (read), EPI_GELU: H (written)
+  const __nv_bfloat16 *aux;  // EPI_DGELU: H (read directly)
   long long ld_aux;
   float alpha;
+  int num_m, num_n;        // tile grid
 };
+
+// Output staging per epilogue warp: a 32 x 32 box (bf16 C [+ bf16 H], or fp32 C).
+constexpr int kStageBytes = 32 * 32 * 4;
 
 template <int BN>
 struct Smem {
   alignas(1024) __nv_bfloat16 a[kStages][BM * BK];
   alignas(1024) __nv_bfloat16 b[kStages][BN * BK];
+  alignas(128) unsigned char out[4][kStageBytes];
   uint64_t full[kStages];
   uint64_t empty[kStages];
-  uint64_t tmem_full;
+  uint64_t tmem_full[2];
+  uint64_t tmem_empty[2];
   uint32_t tmem_base;
 };
 
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, const void *smem_src, int c0,
+                                             int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(smem_u32(smem_src))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Persistent, warp-specialized: warp 0 streams operand tiles (TMA) through a
+// kStages ring, warp 1 issues tcgen05.mma into one of two TMEM accumulators
+// (2 x BN columns), warps 2-5 drain the other accumulator (tcgen05.ld ->
+// fused epilogue -> smem -> TMA store) so the epilogue of tile i overlaps the
+// MMAs of tile i+1.
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+            const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_h,
             Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // align the dynamic smem base to 1024 B (swizzle-128B atoms)
   const uint32_t base = smem_u32(smem_raw);
   unsigned char *aligned = smem_raw + ((1024u - (base & 1023u)) & 1023u);
   Smem<BN> &sm = *reinterpret_cast<Smem<BN> *>(aligned);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM;
-  const int n0 = blockIdx.x * BN;
   const int nk = (p.K + BK - 1) / BK;
+  const int num_tiles = p.num_m * p.num_n;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], 1);
     }
-    mbar_init(&sm.tmem_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&sm.tmem_full[a], 1);
+      mbar_init(&sm.tmem_empty[a], 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) {  // TMEM: BN fp32 columns x 128 lanes
+  if (warp == 1) {  // TMEM: two BN-column fp32 accumulators x 128 lanes
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&sm.tmem_base)),
-                 "r"(BN));
+                 "r"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -190,24 +212,28 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     if (lane == 0) {
       // ---- TMA producer ----
       const uint32_t stage_bytes = (BM + BN) * BK * 2;
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kStages;
-        mbar_wait(&sm.empty[s], ((kb / kStages) & 1) ^ 1);
-        mbar_expect_tx(&sm.full[s], stage_bytes);
-        const int k0 = kb * BK;
-        if (!p.a_mn) {
-          tma_load_2d(sm.a[s], &map_a, k0, m0, &sm.full[s]);
-        } else {
+      int it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int m0 = (t % p.num_m) * BM, n0 = (t / p.num_m) * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kStages;
+          mbar_wait(&sm.empty[s], ((it / kStages) & 1) ^ 1);
+          mbar_expect_tx(&sm.full[s], stage_bytes);
+          const int k0 = kb * BK;
+          if (!p.a_mn) {
+            tma_load_2d(sm.a[s], &map_a, k0, m0, &sm.full[s]);
+          } else {
 #pragma unroll
-          for (int j = 0; j < BM / 64; ++j)
-            tma_load_2d(sm.a[s] + j * 64 * BK, &map_a, m0 + 64 * j, k0, &sm.full[s]);
-        }
-        if (!p.b_mn) {
-          tma_load_2d(sm.b[s], &map_b, k0, n0, &sm.full[s]);
-        } else {
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_2d(sm.a[s] + j * 64 * BK, &map_a, m0 + 64 * j, k0, &sm.full[s]);
+          }
+          if (!p.b_mn) {
+            tma_load_2d(sm.b[s], &map_b, k0, n0, &sm.full[s]);
+          } else {
 #pragma unroll
-          for (int j = 0; j < BN / 64; ++j)
-            tma_load_2d(sm.b[s] + j * 64 * BK, &map_b, n0 + 64 * j, k0, &sm.full[s]);
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(sm.b[s] + j * 64 * BK, &map_b, n0 + 64 * j, k0, &sm.full[s]);
+          }
         }
       }
     }
@@ -220,91 +246,144 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       // 1024 B apart (SBO); K advance +2048 B per k16.
       const uint32_t a_lbo = p.a_mn ? BK * 128 : 16, b_lbo = p.b_mn ? BK * 128 : 16;
       const uint32_t k_step_a = p.a_mn ? 2048u : 32u, k_step_b = p.b_mn ? 2048u : 32u;
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kStages;
-        mbar_wait(&sm.full[s], (kb / kStages) & 1);
+      int it = 0, local = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+        const int acc = local & 1;
+        mbar_wait(&sm.tmem_empty[acc], ((local >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t a_addr = smem_u32(sm.a[s]), b_addr = smem_u32(sm.b[s]);
+        const uint32_t d = tmem + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kStages;
+          mbar_wait(&sm.full[s], (it / kStages) & 1);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sm.a[s]), b_addr = smem_u32(sm.b[s]);
 #pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk) {
-          const uint64_t ad = smem_desc(a_addr + kk * k_step_a, a_lbo, 1024);
-          const uint64_t bd = smem_desc(b_addr + kk * k_step_b, b_lbo, 1024);
-          tc_mma(tmem, ad, bd, idesc, (kb | kk) ? 1u : 0u);
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = smem_desc(a_addr + kk * k_step_a, a_lbo, 1024);
+            const uint64_t bd = smem_desc(b_addr + kk * k_step_b, b_lbo, 1024);
+            tc_mma(d, ad, bd, idesc, (kb | kk) ? 1u : 0u);
+          }
+          tc_commit(&sm.empty[s]);  // frees the stage once these MMAs have read it
         }
-        tc_commit(&sm.empty[s]);  // frees the stage once these MMAs have read it
+        tc_commit(&sm.tmem_full[acc]);
       }
-      tc_commit(&sm.tmem_full);
     }
   } else {
-    // ---- epilogue: TMEM -> registers -> fused op -> global ----
-    const int q = warp & 3;                      // TMEM lane quarter this warp may access
-    const int row = m0 + q * 32 + lane;
-    mbar_wait(&sm.tmem_full, 0);
-    tc_fence_after();
-    const bool row_ok = row < p.M;
+    // ---- epilogue: TMEM -> registers -> fused op -> smem -> TMA store ----
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    unsigned char *stage = sm.out[q];
+    int local = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const int m0 = (t % p.num_m) * BM, n0 = (t / p.num_m) * BN;
+      const int row0 = m0 + q * 32;
+      const int row = row0 + lane;
+      mbar_wait(&sm.tmem_full[acc], (local >> 1) & 1);
+      tc_fence_after();
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      uint32_t v[32];
-      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, "
-          "%10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, "
-          "%27, %28, %29, %30, %31}, [%32];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-            "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
-            "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-            "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
-            "=r"(v[31])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (!row_ok) continue;
-      const int col0 = n0 + c;
-      if (col0 >= p.N) continue;
-      const int ncols = min(32, p.N - col0);
-      float f[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]) * p.alpha;
-      if (p.epi == EPI_GELU) {
-        __nv_bfloat16 *h = const_cast<__nv_bfloat16 *>(p.aux) + (long long)row * p.ld_aux + col0;
-        for (int j = 0; j < ncols; ++j) {
-          h[j] = __float2bfloat16_rn(f[j]);
-          f[j] = gelu_f(__bfloat162float(h[j]));
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, "
+            "%10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, "
+            "%27, %28, %29, %30, %31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+              "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+              "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+              "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c + 32 >= BN) {
+          // all of this accumulator has been read: hand it back to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.tmem_empty[acc]);
         }
-      } else if (p.epi == EPI_DGELU) {
-        const __nv_bfloat16 *h = p.aux + (long long)row * p.ld_aux + col0;
-        for (int j = 0; j < ncols; ++j) f[j] *= gelu_grad_f(__bfloat162float(h[j]));
-      }
-      if (p.c_f32) {
-        float *out = reinterpret_cast<float *>(p.C) + (long long)row * p.ldc + col0;
-        for (int j = 0; j < ncols; ++j) out[j] = f[j];
-      } else {
-        __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(p.C) + (long long)row * p.ldc + col0;
-        if (ncols == 32 && ((reinterpret_cast<uintptr_t>(out) & 15u) == 0)) {
+        const int col0 = n0 + c;
+        if (col0 >= p.N || row0 >= p.M) continue;  // warp-uniform: nothing of this box is stored
+        float f[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]) * p.alpha;
+        // the previous TMA store of this warp must have finished reading `stage`
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        if (p.epi == EPI_GELU) {
+          // H = bf16(acc) (kept for the backward), Y = GeLU(H)
+          uint4 *hs = reinterpret_cast<uint4 *>(stage + 2048 + lane * 64);
+          uint4 *ys = reinterpret_cast<uint4 *>(stage + lane * 64);
 #pragma unroll
           for (int j = 0; j < 32; j += 8) {
-            uint4 w;
-            __nv_bfloat162 t0 = __floats2bfloat162_rn(f[j], f[j + 1]);
-            __nv_bfloat162 t1 = __floats2bfloat162_rn(f[j + 2], f[j + 3]);
-            __nv_bfloat162 t2 = __floats2bfloat162_rn(f[j + 4], f[j + 5]);
-            __nv_bfloat162 t3 = __floats2bfloat162_rn(f[j + 6], f[j + 7]);
-            w.x = *reinterpret_cast<uint32_t *>(&t0);
-            w.y = *reinterpret_cast<uint32_t *>(&t1);
-            w.z = *reinterpret_cast<uint32_t *>(&t2);
-            w.w = *reinterpret_cast<uint32_t *>(&t3);
-            *reinterpret_cast<uint4 *>(out + j) = w;
+            uint32_t hw[4], yw[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 hh = __floats2bfloat162_rn(f[j + 2 * e], f[j + 2 * e + 1]);
+              const float2 hf = __bfloat1622float2(hh);
+              __nv_bfloat162 yy = __floats2bfloat162_rn(gelu_f(hf.x), gelu_f(hf.y));
+              hw[e] = *reinterpret_cast<uint32_t *>(&hh);
+              yw[e] = *reinterpret_cast<uint32_t *>(&yy);
+            }
+            hs[j / 8] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            ys[j / 8] = make_uint4(yw[0], yw[1], yw[2], yw[3]);
           }
         } else {
-          for (int j = 0; j < ncols; ++j) out[j] = __float2bfloat16_rn(f[j]);
+          if (p.epi == EPI_DGELU && row < p.M) {
+            const __nv_bfloat16 *h = p.aux + (long long)row * p.ld_aux + col0;
+            const int nc = min(32, p.N - col0);
+            if (nc == 32 && !(reinterpret_cast<uintptr_t>(h) & 15u)) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) {
+                const uint4 w = __ldg(reinterpret_cast<const uint4 *>(h + j));
+                const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 hf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&ww[e]));
+                  f[j + 2 * e] *= gelu_grad_f(hf.x);
+                  f[j + 2 * e + 1] *= gelu_grad_f(hf.y);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j < nc) f[j] *= gelu_grad_f(__bfloat162float(h[j]));
+            }
+          }
+          if (p.c_f32) {
+            float4 *cs = reinterpret_cast<float4 *>(stage + lane * 128);
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) cs[j / 4] = make_float4(f[j], f[j + 1], f[j + 2], f[j + 3]);
+          } else {
+            uint4 *cs = reinterpret_cast<uint4 *>(stage + lane * 64);
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              uint32_t w[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                __nv_bfloat162 tt = __floats2bfloat162_rn(f[j + 2 * e], f[j + 2 * e + 1]);
+                w[e] = *reinterpret_cast<uint32_t *>(&tt);
+              }
+              cs[j / 8] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&map_c, stage, col0, row0);  // TMA clips rows >= M, cols >= N
+          if (p.epi == EPI_GELU) tma_store_2d(&map_h, stage + 2048, col0, row0);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
       }
     }
-    tc_fence_before();
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
+  tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
   }
 }
 
@@ -330,21 +409,22 @@ static EncodeFn encode_fn() {
   return fn;
 }
 
-// 2-D bf16 tensor map: inner (contiguous) extent `inner`, outer extent `outer`,
-// row pitch `ld` elements, box {64, box_outer}, 128B swizzle, OOB -> 0.
-static int make_map(CUtensorMap *m, const void *ptr, long long inner, long long outer,
-                    long long ld, int box_outer) {
+// 2-D tensor map over a row-major [outer][ld] array with logical inner extent
+// `inner`: box {box_inner, box_outer}.
+static int make_map(CUtensorMap *m, const void *ptr, CUtensorMapDataType dt, int esize,
+                    long long inner, long long outer, long long ld, int box_inner, int box_outer,
+                    CUtensorMapSwizzle swz) {
   EncodeFn enc = encode_fn();
   if (!enc) return fail(NTP_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  if ((reinterpret_cast<uintptr_t>(ptr) & 15u) || ((ld * 2) & 15))
-    return fail(NTP_EINVAL, "GEMM operands need 16-byte aligned base and row pitch");
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15u) || ((ld * esize) & 15))
+    return fail(NTP_EINVAL, "GEMM tensors need 16-byte aligned bases and row pitches");
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
-  cuuint32_t box[2] = {64u, (cuuint32_t)box_outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * esize)};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
   cuuint32_t es[2] = {1u, 1u};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides,
-                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(m, dt, 2, const_cast<void *>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     char b[96];
     snprintf(b, sizeof b, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -353,16 +433,40 @@ static int make_map(CUtensorMap *m, const void *ptr, long long inner, long long 
   return NTP_OK;
 }
 
+static int sm_count_dev() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!cache[dev & 63]) {
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev & 63] = n;
+  }
+  return cache[dev & 63];
+}
+
 template <int BN>
 static int launch(const void *A, long long lda, int a_mn, const void *B, long long ldb, int b_mn,
-                  const Params &p, cudaStream_t s) {
-  CUtensorMap ma, mb;
+                  void *C, long long ldc, void *H, long long ldh, Params p, cudaStream_t s) {
+  CUtensorMap ma, mb, mc, mh;
+  const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const auto SW = CU_TENSOR_MAP_SWIZZLE_128B, NOSW = CU_TENSOR_MAP_SWIZZLE_NONE;
   int st;
   // A is logically [M x K]: K-major stored [M][lda], MN-major stored [K][lda]
-  if ((st = a_mn ? make_map(&ma, A, p.M, p.K, lda, BK) : make_map(&ma, A, p.K, p.M, lda, BM)))
+  if ((st = a_mn ? make_map(&ma, A, BF, 2, p.M, p.K, lda, 64, BK, SW)
+                 : make_map(&ma, A, BF, 2, p.K, p.M, lda, 64, BM, SW)))
     return st;
-  if ((st = b_mn ? make_map(&mb, B, p.N, p.K, ldb, BK) : make_map(&mb, B, p.K, p.N, ldb, BN)))
+  if ((st = b_mn ? make_map(&mb, B, BF, 2, p.N, p.K, ldb, 64, BK, SW)
+                 : make_map(&mb, B, BF, 2, p.K, p.N, ldb, 64, BN, SW)))
     return st;
+  if ((st = p.c_f32 ? make_map(&mc, C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.N, p.M, ldc, 32, 32, NOSW)
+                    : make_map(&mc, C, BF, 2, p.N, p.M, ldc, 32, 32, NOSW)))
+    return st;
+  if (p.epi == EPI_GELU) {
+    if ((st = make_map(&mh, H, BF, 2, p.N, p.M, ldh, 32, 32, NOSW))) return st;
+  } else {
+    mh = mc;
+  }
   const int smem = (int)sizeof(Smem<BN>) + 1024;
   static std::once_flag once[64];
   int dev = 0;
@@ -370,8 +474,11 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
   std::call_once(once[dev & 63], [&] {
     cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   });
-  dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM);
-  gemm_kernel<BN><<<grid, kThreads, smem, s>>>(ma, mb, p);
+  p.num_m = (p.M + BM - 1) / BM;
+  p.num_n = (p.N + BN - 1) / BN;
+  const int tiles = p.num_m * p.num_n;
+  const int grid = tiles < sm_count_dev() ? tiles : sm_count_dev();
+  gemm_kernel<BN><<<grid, kThreads, smem, s>>>(ma, mb, mc, mh, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(NTP_ECUDA, std::string("gemm launch: ") + cudaGetErrorString(e));
   return NTP_OK;
@@ -391,9 +498,11 @@ extern "C" int ntp_gemm_bf16(const void *A, int64_t lda, int a_mn, const void *B
     return fail(NTP_EINVAL, "GEMM extent too large");
   if (epilogue < 0 || epilogue > 2) return fail(NTP_EINVAL, "unknown GEMM epilogue");
   if (epilogue != gemm::EPI_NONE && !aux) return fail(NTP_EINVAL, "epilogue needs an aux tensor");
-  gemm::Params p{(int)M, (int)N, (int)K, a_mn ? 1 : 0, b_mn ? 1 : 0, C, ldc, c_f32 ? 1 : 0,
-                 epilogue, static_cast<const __nv_bfloat16 *>(aux), ld_aux, alpha};
+  if (epilogue == gemm::EPI_GELU && c_f32) return fail(NTP_EINVAL, "GeLU epilogue writes bf16");
+  gemm::Params p{(int)M, (int)N, (int)K, a_mn ? 1 : 0, b_mn ? 1 : 0, c_f32 ? 1 : 0, epilogue,
+                 static_cast<const __nv_bfloat16 *>(aux), ld_aux, alpha, 0, 0};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (N > 128) return gemm::launch<256>(A, lda, a_mn, B, ldb, b_mn, p, s);
-  return gemm::launch<128>(A, lda, a_mn, B, ldb, b_mn, p, s);
+  void *H = const_cast<void *>(aux);
+  if (N > 128) return gemm::launch<256>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
+  return gemm::launch<128>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
 }
