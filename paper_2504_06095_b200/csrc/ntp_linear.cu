@@ -138,7 +138,28 @@ struct Params {
   long long ld_aux;
   float alpha;
   int num_m, num_n;        // tile grid
+  void *C, *H;             // outputs (H: EPI_GELU pre-activation)
+  long long ldc, ldh;
+  int c_tma, h_tma;        // 1: 16-byte aligned pitch -> TMA store; 0: warp copy
 };
+
+// Copy a staged 32 x 32 box to global with row/column masking (pitches a TMA
+// map cannot describe).  esize = 2 (bf16) or 4 (fp32).
+__device__ __forceinline__ void box_store(const unsigned char *stage, void *g, long long ld,
+                                          int esize, int row0, int col0, int M, int N, int lane) {
+  const int col = col0 + lane;
+  if (col >= N) return;
+  for (int r = 0; r < 32; ++r) {
+    const int row = row0 + r;
+    if (row >= M) break;
+    if (esize == 4)
+      reinterpret_cast<float *>(g)[(long long)row * ld + col] =
+          reinterpret_cast<const float *>(stage)[r * 32 + lane];
+    else
+      reinterpret_cast<__nv_bfloat16 *>(g)[(long long)row * ld + col] =
+          reinterpret_cast<const __nv_bfloat16 *>(stage)[r * 32 + lane];
+  }
+}
 
 // Output staging per epilogue warp: a 32 x 32 box (bf16 C [+ bf16 H], or fp32 C).
 constexpr int kStageBytes = 32 * 32 * 4;
@@ -371,10 +392,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&map_c, stage, col0, row0);  // TMA clips rows >= M, cols >= N
-          if (p.epi == EPI_GELU) tma_store_2d(&map_h, stage + 2048, col0, row0);
+          if (p.c_tma) tma_store_2d(&map_c, stage, col0, row0);  // TMA clips rows >= M, cols >= N
+          if (p.epi == EPI_GELU && p.h_tma) tma_store_2d(&map_h, stage + 2048, col0, row0);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
+        if (!p.c_tma) box_store(stage, p.C, p.ldc, p.c_f32 ? 4 : 2, row0, col0, p.M, p.N, lane);
+        if (p.epi == EPI_GELU && !p.h_tma)
+          box_store(stage + 2048, p.H, p.ldh, 2, row0, col0, p.M, p.N, lane);
+        __syncwarp();
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -459,14 +484,20 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
   if ((st = b_mn ? make_map(&mb, B, BF, 2, p.N, p.K, ldb, 64, BK, SW)
                  : make_map(&mb, B, BF, 2, p.K, p.N, ldb, 64, BN, SW)))
     return st;
-  if ((st = p.c_f32 ? make_map(&mc, C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.N, p.M, ldc, 32, 32, NOSW)
-                    : make_map(&mc, C, BF, 2, p.N, p.M, ldc, 32, 32, NOSW)))
+  const int ce = p.c_f32 ? 4 : 2;
+  p.C = C;
+  p.H = H;
+  p.ldc = ldc;
+  p.ldh = ldh;
+  p.c_tma = !((reinterpret_cast<uintptr_t>(C) & 15u) || ((ldc * ce) & 15));
+  p.h_tma = p.epi == EPI_GELU && !((reinterpret_cast<uintptr_t>(H) & 15u) || ((ldh * 2) & 15));
+  memset(&mc, 0, sizeof mc);
+  memset(&mh, 0, sizeof mh);
+  if (p.c_tma && (st = p.c_f32 ? make_map(&mc, C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.N, p.M, ldc,
+                                          32, 32, NOSW)
+                               : make_map(&mc, C, BF, 2, p.N, p.M, ldc, 32, 32, NOSW)))
     return st;
-  if (p.epi == EPI_GELU) {
-    if ((st = make_map(&mh, H, BF, 2, p.N, p.M, ldh, 32, 32, NOSW))) return st;
-  } else {
-    mh = mc;
-  }
+  if (p.h_tma && (st = make_map(&mh, H, BF, 2, p.N, p.M, ldh, 32, 32, NOSW))) return st;
   const int smem = (int)sizeof(Smem<BN>) + 1024;
   static std::once_flag once[64];
   int dev = 0;
@@ -500,7 +531,8 @@ extern "C" int ntp_gemm_bf16(const void *A, int64_t lda, int a_mn, const void *B
   if (epilogue != gemm::EPI_NONE && !aux) return fail(NTP_EINVAL, "epilogue needs an aux tensor");
   if (epilogue == gemm::EPI_GELU && c_f32) return fail(NTP_EINVAL, "GeLU epilogue writes bf16");
   gemm::Params p{(int)M, (int)N, (int)K, a_mn ? 1 : 0, b_mn ? 1 : 0, c_f32 ? 1 : 0, epilogue,
-                 static_cast<const __nv_bfloat16 *>(aux), ld_aux, alpha, 0, 0};
+                 static_cast<const __nv_bfloat16 *>(aux), ld_aux, alpha, 0, 0,
+                 nullptr, nullptr, 0, 0, 0, 0};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   void *H = const_cast<void *>(aux);
   if (N > 128) return gemm::launch<256>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
