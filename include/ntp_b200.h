@@ -58,8 +58,9 @@ int ntp_abi_version(void);
 /* Process-wide tuning knobs (no reference counterpart). */
 enum ntp_option { NTP_OPT_SYNC_KERNEL = 0 };
 enum ntp_sync_kernel {
+  NTP_KERNEL_AUTO = 0,  /* default: LDG below 4 chunks per SM, BULK above */
   NTP_KERNEL_LDG = 1,   /* 128-bit register-staged loads/stores */
-  NTP_KERNEL_BULK = 2,  /* TMA bulk copies through shared memory, 4 stages, 1 CTA/SM (default) */
+  NTP_KERNEL_BULK = 2,  /* TMA bulk copies through shared memory, 4 stages, 1 CTA/SM */
   NTP_KERNEL_BULK2 = 3  /* TMA bulk copies, 3 stages, 2 CTAs/SM */
 };
 int ntp_set_option(int option, int64_t value);

@@ -515,7 +515,7 @@ static int grid_for(K kernel, int device, int n_items) {
   return n_items < g ? (n_items > 0 ? n_items : 1) : g;
 }
 
-static std::atomic<int> g_sync_kernel{NTP_KERNEL_BULK};
+static std::atomic<int> g_sync_kernel{NTP_KERNEL_AUTO};
 
 template <typename T, int OP, int kStages, bool kSig>
 static int launch_bulk(const ntp_plan *p, const BufTable &bt, typename Acc<T>::type wa,
@@ -540,7 +540,9 @@ static int launch_plan_t(const ntp_plan *p, const BufTable &bt, double wa, doubl
                          const SignalArgs &sig, cudaStream_t s) {
   using A = typename Acc<T>::type;
   const int n = (int)p->chunks.size();
-  const int variant = g_sync_kernel.load();
+  int variant = g_sync_kernel.load();
+  if (variant == NTP_KERNEL_AUTO)  // small plans are latency-bound: no smem pipeline fill
+    variant = n < 4 * sm_count(p->device) ? NTP_KERNEL_LDG : NTP_KERNEL_BULK;
   if (p->vectorized && (variant == NTP_KERNEL_BULK || variant == NTP_KERNEL_BULK2)) {
     if (variant == NTP_KERNEL_BULK)
       return launch_bulk<T, OP, 4, kSig>(p, bt, A(wa), A(wb), 1, sig, s);
@@ -612,7 +614,7 @@ extern "C" {
 
 int ntp_set_option(int option, int64_t value) {
   if (option != NTP_OPT_SYNC_KERNEL) return fail(NTP_EINVAL, "unknown option");
-  if (value < NTP_KERNEL_LDG || value > NTP_KERNEL_BULK2)
+  if (value < NTP_KERNEL_AUTO || value > NTP_KERNEL_BULK2)
     return fail(NTP_EINVAL, "unknown sync kernel variant");
   g_sync_kernel.store((int)value);
   return NTP_OK;

@@ -30,7 +30,7 @@ def _max(x: float) -> float:
 def run(args):
     from bench import METRIC, W_H, W_R, ClockSampler, peaks  # noqa: I001 (repo root on sys.path)
 
-    os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
+    os.environ["NCCL_DEBUG"] = os.environ.get("NTP_NCCL_DEBUG", "WARN")  # stdout: one JSON line
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if not dist.is_initialized():

@@ -52,11 +52,18 @@ def sync_sweep_local():
         # small messages fit in L2: flush it between launches by timing a chain
         # long enough that the data set is re-streamed; report both honestly
         iters = max(5, min(2000, int(2e9 / (lay.elems * 2))))
-        ms = timed(lambda: plan.grad_sync(ptrs, OPS["weighted"], 4 / 7, 3 / 7), iters)
         b = 4 * lay.elems * 2
-        rows.append({"grad_bytes_per_replica": lay.elems * 2, "k": k, "us": round(ms * 1e3, 2),
-                     "hbm_gbs": round(b / ms / 1e6, 1), "frac_hbm": round(b / ms / 1e6 / HBM, 3),
-                     "note": "L2-resident" if 4 * lay.elems * 2 < 100e6 else "HBM-streamed"})
+        row = {"grad_bytes_per_replica": lay.elems * 2, "k": k,
+               "note": "L2-resident" if b < 100e6 else "HBM-streamed"}
+        L = _lib.load()
+        for name, v in (("auto", 0), ("ldg", 1), ("bulk", 2)):
+            if v:
+                _lib.check(L.ntp_set_option(0, v))
+            ms = timed(lambda: plan.grad_sync(ptrs, OPS["weighted"], 4 / 7, 3 / 7), iters)
+            row[name] = {"us": round(ms * 1e3, 2), "hbm_gbs": round(b / ms / 1e6, 1),
+                         "frac_hbm": round(b / ms / 1e6 / HBM, 3)}
+        _lib.check(L.ntp_set_option(0, 0))
+        rows.append(row)
         del arenas
     return rows
 

@@ -302,4 +302,4 @@ def test_bulk_kernel_variants_match_oracle(T, variant):
                 check(h2, hb, dtype)
                 check(r2, rb, dtype)
     finally:
-        _lib.check(L.ntp_set_option(0, 2))
+        _lib.check(L.ntp_set_option(0, 0))  # back to AUTO
