@@ -211,6 +211,10 @@ int ntp_gemm_bf16(const void *A, int64_t lda, int a_mn, const void *B, int64_t l
                   void *C, int64_t ldc, int c_f32, int64_t M, int64_t N, int64_t K, int epilogue,
                   const void *aux, int64_t ld_aux, float alpha, void *stream);
 
+/* 1 (default): N > 128 uses 256 x 256 tiles on CTA pairs (tcgen05.mma.cta_group::2,
+ * cluster of 2); 0: 128 x 256 tiles on single CTAs. */
+int ntp_gemm_set_pair(int on);
+
 /* ------------------------------------------------------------------------
  * Multi-GPU plumbing: peer memory over NVLink/NVSwitch and device signals
  * ------------------------------------------------------------------------ */

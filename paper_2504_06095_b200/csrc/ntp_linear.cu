@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -164,13 +165,13 @@ __device__ __forceinline__ void box_store(const unsigned char *stage, void *g, l
 // Output staging per epilogue warp: a 32 x 32 box (bf16 C [+ bf16 H], or fp32 C).
 constexpr int kStageBytes = 32 * 32 * 4;
 
-template <int BN>
+template <int BN, int kPair, int kStg>
 struct Smem {
-  alignas(1024) __nv_bfloat16 a[kStages][BM * BK];
-  alignas(1024) __nv_bfloat16 b[kStages][BN * BK];
+  alignas(1024) __nv_bfloat16 a[kStg][BM * BK];
+  alignas(1024) __nv_bfloat16 b[kStg][(BN / kPair) * BK];
   alignas(128) unsigned char out[4][kStageBytes];
-  uint64_t full[kStages];
-  uint64_t empty[kStages];
+  uint64_t full[kStg];
+  uint64_t empty[kStg];
   uint64_t tmem_full[2];
   uint64_t tmem_empty[2];
   uint32_t tmem_base;
@@ -186,13 +187,57 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, const void 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// arrive on the barrier at the same smem offset in cluster CTA `rank`
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t *bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+// 2-SM TMA load: bytes land in this CTA's smem, completion is counted on the
+// leader CTA's barrier (peer bit cleared), as CUTLASS's SM100_TMA_2SM_LOAD.
+__device__ __forceinline__ void tma_load_2d_pair(void *smem_dst, const CUtensorMap *map, int c0,
+                                                 int c1, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit2(uint64_t *bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
 
 // Persistent, warp-specialized: warp 0 streams operand tiles (TMA) through a
-// kStages ring, warp 1 issues tcgen05.mma into one of two TMEM accumulators
+// kStg ring, warp 1 issues tcgen05.mma into one of two TMEM accumulators
 // (2 x BN columns), warps 2-5 drain the other accumulator (tcgen05.ld ->
 // fused epilogue -> smem -> TMA store) so the epilogue of tile i overlaps the
-// MMAs of tile i+1.
-template <int BN>
+// MMAs of tile i+1.  kPair = 2: a CTA pair (cluster of 2) computes a 256 x BN
+// tile with tcgen05.mma.cta_group::2 -- each CTA stages its 128 rows of A and
+// half of B, the leader issues the MMAs, both drain their own TMEM half.
+template <int BN, int kPair, int kStg>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
             const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_h,
@@ -200,93 +245,110 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t base = smem_u32(smem_raw);
   unsigned char *aligned = smem_raw + ((1024u - (base & 1023u)) & 1023u);
-  Smem<BN> &sm = *reinterpret_cast<Smem<BN> *>(aligned);
+  Smem<BN, kPair, kStg> &sm = *reinterpret_cast<Smem<BN, kPair, kStg> *>(aligned);
+  constexpr int BNC = BN / kPair;  // B rows staged by this CTA
+  constexpr int TM = BM * kPair;   // tile rows of the pair
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nk = (p.K + BK - 1) / BK;
   const int num_tiles = p.num_m * p.num_n;
+  const uint32_t rank = kPair == 2 ? cluster_rank() : 0u;
+  const bool leader = rank == 0;
+  const int unit_id = blockIdx.x / kPair, num_units = gridDim.x / kPair;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kStg; ++s) {
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&sm.tmem_full[a], 1);
-      mbar_init(&sm.tmem_empty[a], 4);  // one arrive per epilogue warp
+      mbar_init(&sm.tmem_empty[a], 4 * kPair);  // one arrive per epilogue warp of the pair
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {  // TMEM: two BN-column fp32 accumulators x 128 lanes
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&sm.tmem_base)),
-                 "r"(2 * BN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (kPair == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&sm.tmem_base)),
+                   "r"(2 * BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&sm.tmem_base)),
+                   "r"(2 * BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---- TMA producer ----
-      const uint32_t stage_bytes = (BM + BN) * BK * 2;
+      // ---- TMA producer (both CTAs of a pair) ----
+      const uint32_t cta_bytes = (BM + BNC) * BK * 2;
       int it = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int m0 = (t % p.num_m) * BM, n0 = (t / p.num_m) * BN;
+      for (int t = unit_id; t < num_tiles; t += num_units) {
+        const int m0 = (t % p.num_m) * TM + (int)rank * BM;
+        const int n0 = (t / p.num_m) * BN + (int)rank * BNC;
         for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % kStages;
-          mbar_wait(&sm.empty[s], ((it / kStages) & 1) ^ 1);
-          mbar_expect_tx(&sm.full[s], stage_bytes);
+          const int s = it % kStg;
+          mbar_wait(&sm.empty[s], ((it / kStg) & 1) ^ 1);
+          if (leader) mbar_expect_tx(&sm.full[s], cta_bytes * kPair);
           const int k0 = kb * BK;
+          auto load = [&](void *dst, const CUtensorMap *m, int c0, int c1) {
+            if constexpr (kPair == 2) tma_load_2d_pair(dst, m, c0, c1, &sm.full[s]);
+            else tma_load_2d(dst, m, c0, c1, &sm.full[s]);
+          };
           if (!p.a_mn) {
-            tma_load_2d(sm.a[s], &map_a, k0, m0, &sm.full[s]);
+            load(sm.a[s], &map_a, k0, m0);
           } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j)
-              tma_load_2d(sm.a[s] + j * 64 * BK, &map_a, m0 + 64 * j, k0, &sm.full[s]);
+            for (int j = 0; j < BM / 64; ++j) load(sm.a[s] + j * 64 * BK, &map_a, m0 + 64 * j, k0);
           }
           if (!p.b_mn) {
-            tma_load_2d(sm.b[s], &map_b, k0, n0, &sm.full[s]);
+            load(sm.b[s], &map_b, k0, n0);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d(sm.b[s] + j * 64 * BK, &map_b, n0 + 64 * j, k0, &sm.full[s]);
+            for (int j = 0; j < BNC / 64; ++j) load(sm.b[s] + j * 64 * BK, &map_b, n0 + 64 * j, k0);
           }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---- MMA issuer ----
-      const uint32_t idesc = instr_desc(BM, BN, p.a_mn, p.b_mn);
+    if (lane == 0 && leader) {
+      // ---- MMA issuer (the leader CTA of a pair) ----
+      const uint32_t idesc = instr_desc(TM, BN, p.a_mn, p.b_mn);
       // K-major: rows of 128 B, 8-row atoms 1024 B apart (SBO); K advance +32 B per k16.
       // MN-major: 64-element MN blocks of BK rows (LBO = BK*128 B), 8-row K groups
       // 1024 B apart (SBO); K advance +2048 B per k16.
       const uint32_t a_lbo = p.a_mn ? BK * 128 : 16, b_lbo = p.b_mn ? BK * 128 : 16;
       const uint32_t k_step_a = p.a_mn ? 2048u : 32u, k_step_b = p.b_mn ? 2048u : 32u;
       int it = 0, local = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+      for (int t = unit_id; t < num_tiles; t += num_units, ++local) {
         const int acc = local & 1;
         mbar_wait(&sm.tmem_empty[acc], ((local >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(acc * BN);
         for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % kStages;
-          mbar_wait(&sm.full[s], (it / kStages) & 1);
+          const int s = it % kStg;
+          mbar_wait(&sm.full[s], (it / kStg) & 1);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sm.a[s]), b_addr = smem_u32(sm.b[s]);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ad = smem_desc(a_addr + kk * k_step_a, a_lbo, 1024);
             const uint64_t bd = smem_desc(b_addr + kk * k_step_b, b_lbo, 1024);
-            tc_mma(d, ad, bd, idesc, (kb | kk) ? 1u : 0u);
+            if constexpr (kPair == 2) tc_mma2(d, ad, bd, idesc, (kb | kk) ? 1u : 0u);
+            else tc_mma(d, ad, bd, idesc, (kb | kk) ? 1u : 0u);
           }
-          tc_commit(&sm.empty[s]);  // frees the stage once these MMAs have read it
+          // frees the stage (in both CTAs) once these MMAs have read it
+          if constexpr (kPair == 2) tc_commit2(&sm.empty[s], 0x3); else tc_commit(&sm.empty[s]);
         }
-        tc_commit(&sm.tmem_full[acc]);
+        if constexpr (kPair == 2) tc_commit2(&sm.tmem_full[acc], 0x3); else tc_commit(&sm.tmem_full[acc]);
       }
     }
   } else {
@@ -294,9 +356,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     unsigned char *stage = sm.out[q];
     int local = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+    for (int t = unit_id; t < num_tiles; t += num_units, ++local) {
       const int acc = local & 1;
-      const int m0 = (t % p.num_m) * BM, n0 = (t / p.num_m) * BN;
+      const int m0 = (t % p.num_m) * TM + (int)rank * BM, n0 = (t / p.num_m) * BN;
       const int row0 = m0 + q * 32;
       const int row = row0 + lane;
       mbar_wait(&sm.tmem_full[acc], (local >> 1) & 1);
@@ -321,7 +383,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
           // all of this accumulator has been read: hand it back to the MMA warp
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.tmem_empty[acc]);
+          if (lane == 0) {
+            if constexpr (kPair == 2) mbar_arrive_cluster(&sm.tmem_empty[acc], 0);
+            else mbar_arrive(&sm.tmem_empty[acc]);
+          }
         }
         const int col0 = n0 + c;
         if (col0 >= p.N || row0 >= p.M) continue;  // warp-uniform: nothing of this box is stored
@@ -405,10 +470,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+    if constexpr (kPair == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
   }
 }
 
@@ -470,9 +538,10 @@ static int sm_count_dev() {
   return cache[dev & 63];
 }
 
-template <int BN>
+template <int BN, int kPair, int kStg>
 static int launch(const void *A, long long lda, int a_mn, const void *B, long long ldb, int b_mn,
                   void *C, long long ldc, void *H, long long ldh, Params p, cudaStream_t s) {
+  constexpr int BNC = BN / kPair;
   CUtensorMap ma, mb, mc, mh;
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const auto SW = CU_TENSOR_MAP_SWIZZLE_128B, NOSW = CU_TENSOR_MAP_SWIZZLE_NONE;
@@ -482,7 +551,7 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
                  : make_map(&ma, A, BF, 2, p.K, p.M, lda, 64, BM, SW)))
     return st;
   if ((st = b_mn ? make_map(&mb, B, BF, 2, p.N, p.K, ldb, 64, BK, SW)
-                 : make_map(&mb, B, BF, 2, p.K, p.N, ldb, 64, BN, SW)))
+                 : make_map(&mb, B, BF, 2, p.K, p.N, ldb, 64, BNC, SW)))
     return st;
   const int ce = p.c_f32 ? 4 : 2;
   p.C = C;
@@ -498,22 +567,38 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
                                : make_map(&mc, C, BF, 2, p.N, p.M, ldc, 32, 32, NOSW)))
     return st;
   if (p.h_tma && (st = make_map(&mh, H, BF, 2, p.N, p.M, ldh, 32, 32, NOSW))) return st;
-  const int smem = (int)sizeof(Smem<BN>) + 1024;
+  auto kern = gemm_kernel<BN, kPair, kStg>;
+  const int smem = (int)sizeof(Smem<BN, kPair, kStg>) + 1024;
   static std::once_flag once[64];
   int dev = 0;
   cudaGetDevice(&dev);
   std::call_once(once[dev & 63], [&] {
-    cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   });
-  p.num_m = (p.M + BM - 1) / BM;
+  p.num_m = (p.M + BM * kPair - 1) / (BM * kPair);
   p.num_n = (p.N + BN - 1) / BN;
   const int tiles = p.num_m * p.num_n;
-  const int grid = tiles < sm_count_dev() ? tiles : sm_count_dev();
-  gemm_kernel<BN><<<grid, kThreads, smem, s>>>(ma, mb, mc, mh, p);
-  cudaError_t e = cudaGetLastError();
+  const int units = sm_count_dev() / kPair;
+  const int grid = (tiles < units ? tiles : units) * kPair;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kPair;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mh, p);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(NTP_ECUDA, std::string("gemm launch: ") + cudaGetErrorString(e));
   return NTP_OK;
 }
+
+static std::atomic<int> g_pair{1};
 
 }  // namespace gemm
 }  // namespace ntp
@@ -535,6 +620,16 @@ extern "C" int ntp_gemm_bf16(const void *A, int64_t lda, int a_mn, const void *B
                  nullptr, nullptr, 0, 0, 0, 0};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   void *H = const_cast<void *>(aux);
-  if (N > 128) return gemm::launch<256>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
-  return gemm::launch<128>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
+  if (N > 128) {
+    if (gemm::g_pair.load())
+      return gemm::launch<256, 2, 6>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
+    return gemm::launch<256, 1, 4>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
+  }
+  return gemm::launch<128, 1, 4>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
+}
+
+// 1 (default): 256-row CTA-pair tiles (tcgen05 cta_group::2) for N > 128; 0: 1-SM tiles.
+extern "C" int ntp_gemm_set_pair(int on) {
+  gemm::g_pair.store(on ? 1 : 0);
+  return NTP_OK;
 }

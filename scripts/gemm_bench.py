@@ -57,13 +57,18 @@ def main():
             ("wgrad dA_i=D^T X (unit-major)", lambda: L.mm(Db.T, X.T, grads[:, 0, :]),
              lambda: torch.matmul(Db.T, X), n, h, T),
         ]
+        from paper_2504_06095_b200 import _lib
         for name, ours, ref, M, N, K in cases:
             fl = 2.0 * M * N * K
+            _lib.load().ntp_gemm_set_pair(0)
+            ms1 = timed(ours)
+            _lib.load().ntp_gemm_set_pair(1)
             ms = timed(ours)
             ms_ref = timed(ref)
             out["gemms"].append({"n_i": n, "gemm": name, "M": M, "N": N, "K": K,
                                  "ours_ms": round(ms, 4), "ours_tflops": round(fl / ms / 1e9, 1),
                                  "ours_frac": round(fl / ms / 1e9 / PEAK, 3),
+                                 "single_cta_tflops": round(fl / ms1 / 1e9, 1),
                                  "cublas_ms": round(ms_ref, 4),
                                  "cublas_tflops": round(fl / ms_ref / 1e9, 1)})
     print(json.dumps(out, indent=1))
