@@ -156,6 +156,14 @@ void ntp_plan_destroy(ntp_plan *plan);
 int ntp_grad_sync(const ntp_plan *plan, void *const *bufs, int n_bufs, int op, double w_a,
                   double w_b, void *stream);
 
+/* ntp_grad_sync with a write mask: bit 0 writes the result to side A, bit 1 to
+ * side B.  write_mask = 1 accumulates the B replica's (weighted) contribution
+ * into A only -- the first phase of a DP > 2 sync across processes (the degraded
+ * replica's share folded into one healthy replica before the NCCL all-reduce of
+ * the aligned healthy replicas). */
+int ntp_grad_sync_ex(const ntp_plan *plan, void *const *bufs, int n_bufs, int op, double w_a,
+                     double w_b, int write_mask, void *stream);
+
 /* Reconfiguration copy (no reference function; built from build_reshard_plan
  * 185-206 / apply_plan 209-217 / contiguous_assignment tpnumerics.py:115-120):
  * B = A for every unit.  Bit-exact. */

@@ -61,6 +61,8 @@ SIGNATURES = {
     "ntp_plan_destroy": (None, [_vp]),
     "ntp_grad_sync": (ctypes.c_int, [_vp, _vpp, ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                      ctypes.c_double, _vp]),
+    "ntp_grad_sync_ex": (ctypes.c_int, [_vp, _vpp, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                        ctypes.c_double, ctypes.c_int, _vp]),
     "ntp_reshard": (ctypes.c_int, [_vp, _vpp, ctypes.c_int, _vp]),
     "ntp_uniform_sync": (ctypes.c_int, [_vpp, ctypes.c_int, ctypes.c_int64, ctypes.c_int,
                                         ctypes.c_int, ctypes.POINTER(ctypes.c_double), _vp]),

@@ -53,6 +53,7 @@ struct SignalArgs {
   uint64_t spin_ns;
   int *status;
   unsigned int *counter;  // CTA completion counter (device, zeroed)
+  int wmask = 3;          // bit 0: write side A, bit 1: write side B
 };
 
 enum { OP_COPY = 3 };
@@ -264,8 +265,8 @@ plan_kernel_vec(const Chunk *__restrict__ chunks, int n_chunks, BufTable bufs,
             st_stream(b + i, va[u]);
           } else {
             const uint4 o = VecOp<T, OP>::run(va[u], vb[u], wa, wb);
-            st_stream(a + i, o);
-            st_stream(b + i, o);
+            if (sig.wmask & 1) st_stream(a + i, o);
+            if (sig.wmask & 2) st_stream(b + i, o);
           }
         }
       }
@@ -403,8 +404,12 @@ plan_kernel_bulk(const Chunk *__restrict__ chunks, int n_chunks, BufTable bufs,
     if (tid == 0) {
       uint4 *ga = reinterpret_cast<uint4 *>(bufs.p[rec.w & 0xffffu]) + rec.x;
       uint4 *gb = reinterpret_cast<uint4 *>(bufs.p[rec.w >> 16]) + rec.y;
-      if constexpr (OP != OP_COPY) bulk_store(ga, sm.a[stage], rec.z * 16u);
-      bulk_store(gb, sm.a[stage], rec.z * 16u);
+      if constexpr (OP != OP_COPY) {
+        if (sig.wmask & 1) bulk_store(ga, sm.a[stage], rec.z * 16u);
+        if (sig.wmask & 2) bulk_store(gb, sm.a[stage], rec.z * 16u);
+      } else {
+        bulk_store(gb, sm.a[stage], rec.z * 16u);
+      }
       bulk_commit();
       // the previous stage's stores have finished reading shared memory
       bulk_wait_read<1>();
@@ -443,8 +448,8 @@ plan_kernel_scalar(const Chunk *__restrict__ chunks, int n_chunks, BufTable bufs
         b[i] = a[i];
       } else {
         const T o = combine_scalar<T, OP>(a[i], b[i], wa, wb);
-        a[i] = o;
-        b[i] = o;
+        if (sig.wmask & 1) a[i] = o;
+        if (sig.wmask & 2) b[i] = o;
       }
     }
   }
@@ -661,6 +666,23 @@ int ntp_grad_sync(const ntp_plan *p, void *const *bufs, int n_bufs, int op, doub
   if (p->chunks.empty()) return NTP_OK;
   if ((st = set_device(p->device))) return st;
   SignalArgs sig{};
+  st = launch_plan<false>(p, op, bt, w_a, w_b, sig, static_cast<cudaStream_t>(stream));
+  if (st) return st;
+  NTP_CUDA(cudaGetLastError());
+  return NTP_OK;
+}
+
+int ntp_grad_sync_ex(const ntp_plan *p, void *const *bufs, int n_bufs, int op, double w_a,
+                     double w_b, int write_mask, void *stream) {
+  BufTable bt;
+  int st = check_exec(p, bufs, n_bufs, bt);
+  if (st) return st;
+  if (op < NTP_OP_SUM || op > NTP_OP_WEIGHTED) return fail(NTP_EINVAL, "unknown reduction op");
+  if (write_mask < 1 || write_mask > 3) return fail(NTP_EINVAL, "write_mask must be 1, 2 or 3");
+  if (p->chunks.empty()) return NTP_OK;
+  if ((st = set_device(p->device))) return st;
+  SignalArgs sig{};
+  sig.wmask = write_mask;
   st = launch_plan<false>(p, op, bt, w_a, w_b, sig, static_cast<cudaStream_t>(stream));
   if (st) return st;
   NTP_CUDA(cudaGetLastError());

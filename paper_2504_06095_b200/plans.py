@@ -99,6 +99,13 @@ class Plan:
                                          float(w_b), _stream_ptr(stream, self.device)),
                    "ntp_grad_sync")
 
+    def grad_sync_into(self, bufs, op: int, w_a: float, w_b: float, write_mask: int,
+                       stream=None) -> None:
+        """grad_sync writing only the sides in write_mask (1: A, 2: B, 3: both)."""
+        _lib.check(self._L.ntp_grad_sync_ex(self._h, _lib.ptr_array(bufs), len(bufs), int(op),
+                                            float(w_a), float(w_b), int(write_mask),
+                                            _stream_ptr(stream, self.device)), "ntp_grad_sync_ex")
+
     def reshard(self, bufs, stream=None) -> None:
         ptrs = _lib.ptr_array(bufs)
         _lib.check(self._L.ntp_reshard(self._h, ptrs, len(bufs), _stream_ptr(stream, self.device)),
