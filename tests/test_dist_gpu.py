@@ -38,3 +38,25 @@ def test_four_gpus_tp2_tp1():
 
 def test_eight_gpus_tp4_tp3():
     _run(8, 4, 3, "bf16", 3)
+
+
+def _run_script(n, script, *args):
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + n),
+           os.path.join(ROOT, "scripts", script), *map(str, args)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "PASS" in r.stdout
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_four_gpus_dp3_with_degraded_replica(dtype):
+    """DP=3: two healthy TP2 replicas (one GPU each) + a TP1 replica."""
+    _run_script(4, "dp_check.py", 2, 2, 1, dtype, 2)
+
+
+def test_eight_gpus_c3():
+    """BASELINE configs[2]: DP=4 x TP2 with one replica degraded to TP1 (7 GPUs)."""
+    _run_script(8, "dp_check.py", 3, 2, 1, "bf16", 2)
