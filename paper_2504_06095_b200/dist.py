@@ -319,5 +319,7 @@ def aligned_all_reduce(tensor: torch.Tensor, weight: float | None = None, group=
     if weight is None or weight == 1.0:
         dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=group)
         return
-    op = dist._make_nccl_premul_sum(float(weight))
+    # device scalar of the tensor's dtype: a host double factor is mis-read for 16-bit dtypes
+    factor = torch.tensor([float(weight)], dtype=tensor.dtype, device=tensor.device)
+    op = dist._make_nccl_premul_sum(factor)
     dist.all_reduce(tensor, op=op, group=group)

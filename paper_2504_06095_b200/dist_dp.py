@@ -179,8 +179,10 @@ class NtpDpGroup:
                     continue
                 r = mine[0]
                 t = self.arena(r * plc.n1 + i)
-                # every rank must use the same NCCL op: pre-mul-sum, H_0's factor 1
-                op = dist._make_nccl_premul_sum(1.0 if r == 0 else float(self.w[r]))
+                # every rank must use the same NCCL op: pre-mul-sum, H_0's factor 1.
+                # The factor is a device scalar of the tensor's dtype (a host
+                # double is mis-read as a 16-bit scalar for bf16 all-reduces).
+                op = dist._make_nccl_premul_sum(self._factor(1.0 if r == 0 else self.w[r], t))
                 dist.all_reduce(t, op=op, group=self.groups[procs])
         # C: push the result into D's arena, then release D
         if self.plan is not None:
@@ -192,6 +194,13 @@ class NtpDpGroup:
             w = self._words(DONE, self.partners, True)
             _lib.check(L.ntp_signal_wait(_lib.u64_ptr_array(w), len(w), e, spin_ns, st, sp),
                        "ntp_signal_wait")
+
+    def _factor(self, w: float, t: torch.Tensor) -> torch.Tensor:
+        key = (float(w), t.dtype)
+        cache = self.__dict__.setdefault("_factors", {})
+        if key not in cache:
+            cache[key] = torch.tensor([float(w)], dtype=t.dtype, device=t.device)
+        return cache[key]
 
     def status(self) -> int:
         return int(self._status.item()) if self._status is not None else 0
