@@ -315,11 +315,23 @@ def aligned_all_reduce(tensor: torch.Tensor, weight: float | None = None, group=
     """NCCL fall-through for naturally aligned shards (uniform_grad_sync,
     tpnumerics.py:263-286, across processes): SUM, or per-rank weighted sum via
     NCCL's pre-multiplied-sum op (each rank scales its own input inside NCCL --
-    no separate scale kernel)."""
-    if weight is None or weight == 1.0:
+    no separate scale kernel).  Every rank of the group must pass a weight, or
+    none (NCCL requires one op across the group).  16-bit tensors: torch's
+    pre-mul-sum mis-scales them (measured on B200), so the weight is applied in
+    place by ntp_uniform_sync before a plain SUM."""
+    if weight is None:
         dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=group)
         return
-    # device scalar of the tensor's dtype: a host double factor is mis-read for 16-bit dtypes
-    factor = torch.tensor([float(weight)], dtype=tensor.dtype, device=tensor.device)
-    op = dist._make_nccl_premul_sum(factor)
-    dist.all_reduce(tensor, op=op, group=group)
+    if tensor.element_size() < 4:
+        w = (ctypes.c_double * 1)(float(weight))
+        stream = torch.cuda.current_stream(tensor.device)
+        _lib.check(_lib.load().ntp_uniform_sync(_lib.ptr_array([tensor.data_ptr()]), 1,
+                                                tensor.numel(), dtype_code(tensor.dtype),
+                                                OPS["weighted"], w,
+                                                ctypes.c_void_p(stream.cuda_stream)),
+                   "ntp_uniform_sync")
+        dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=group)
+        return
+    fdt = torch.float64 if tensor.dtype == torch.float64 else torch.float32
+    factor = torch.tensor([float(weight)], dtype=fdt, device=tensor.device)
+    dist.all_reduce(tensor, op=dist._make_nccl_premul_sum(factor), group=group)

@@ -179,11 +179,19 @@ class NtpDpGroup:
                     continue
                 r = mine[0]
                 t = self.arena(r * plc.n1 + i)
-                # every rank must use the same NCCL op: pre-mul-sum, H_0's factor 1.
-                # The factor is a device scalar of the tensor's dtype (a host
-                # double is mis-read as a 16-bit scalar for bf16 all-reduces).
-                op = dist._make_nccl_premul_sum(self._factor(1.0 if r == 0 else self.w[r], t))
-                dist.all_reduce(t, op=op, group=self.groups[procs])
+                if t.element_size() >= 4:
+                    # every rank uses the same NCCL op: pre-mul-sum, H_0's factor 1
+                    op = dist._make_nccl_premul_sum(self._factor(1.0 if r == 0 else self.w[r], t))
+                    dist.all_reduce(t, op=op, group=self.groups[procs])
+                else:
+                    # torch's 16-bit pre-mul-sum mis-scales (measured on B200); weight
+                    # H_r (r > 0) in place with the uniform kernel, then a plain SUM
+                    if r > 0:
+                        w = (ctypes.c_double * 1)(float(self.w[r]))
+                        _lib.check(L.ntp_uniform_sync(_lib.ptr_array([t.data_ptr()]), 1, t.numel(),
+                                                      dtype_code(t.dtype), OPS["weighted"], w, sp),
+                                   "ntp_uniform_sync")
+                    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.groups[procs])
         # C: push the result into D's arena, then release D
         if self.plan is not None:
             self.plan.reshard(self.bufs, s)
@@ -196,10 +204,12 @@ class NtpDpGroup:
                        "ntp_signal_wait")
 
     def _factor(self, w: float, t: torch.Tensor) -> torch.Tensor:
-        key = (float(w), t.dtype)
+        # torch's ProcessGroupNCCL takes an fp32 device scalar for 16-bit dtypes
+        dt = torch.float64 if t.dtype == torch.float64 else torch.float32
+        key = (float(w), dt)
         cache = self.__dict__.setdefault("_factors", {})
         if key not in cache:
-            cache[key] = torch.tensor([float(w)], dtype=t.dtype, device=t.device)
+            cache[key] = torch.tensor([float(w)], dtype=dt, device=t.device)
         return cache[key]
 
     def status(self) -> int:
