@@ -56,7 +56,10 @@ const char *ntp_last_error(void);
 int ntp_abi_version(void);
 
 /* Process-wide tuning knobs (no reference counterpart). */
-enum ntp_option { NTP_OPT_SYNC_KERNEL = 0 };
+enum ntp_option {
+  NTP_OPT_SYNC_KERNEL = 0,   /* value: enum ntp_sync_kernel */
+  NTP_OPT_SYNC_MAX_CTAS = 1  /* value: cap on sync-kernel CTAs, 0 = all SMs */
+};
 enum ntp_sync_kernel {
   NTP_KERNEL_AUTO = 0,  /* default: LDG below 4 chunks per SM, BULK above */
   NTP_KERNEL_LDG = 1,   /* 128-bit register-staged loads/stores */

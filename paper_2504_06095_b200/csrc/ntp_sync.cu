@@ -45,6 +45,10 @@ struct BufTable {
   char *p[kMaxBufs];
 };
 
+// Cap on sync-kernel CTAs (0 = one wave over all SMs).  Lets a sync that is
+// overlapped with the backward GEMMs leave most SMs to the tensor cores.
+static std::atomic<int> g_max_ctas{0};
+
 struct SignalArgs {
   uint64_t *wait[16];
   uint64_t *post[16];
@@ -516,7 +520,9 @@ static int grid_for(K kernel, int device, int n_items) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0) != cudaSuccess ||
       occ <= 0)
     occ = 4;
-  const int g = sm_count(device) * occ;
+  int g = sm_count(device) * occ;
+  const int cap = g_max_ctas.load();
+  if (cap > 0 && g > cap) g = cap;
   return n_items < g ? (n_items > 0 ? n_items : 1) : g;
 }
 
@@ -535,6 +541,8 @@ static int launch_bulk(const ntp_plan *p, const BufTable &bt, typename Acc<T>::t
   });
   const int n = (int)p->chunks.size();
   int grid = sm_count(p->device) * ctas_per_sm;
+  const int cap = g_max_ctas.load();
+  if (cap > 0 && grid > cap) grid = cap;
   if (n < grid) grid = n > 0 ? n : 1;
   k<<<grid, kBulkThreads, smem, s>>>(p->d_chunks, n, bt, wa, wb, sig);
   return NTP_OK;
@@ -618,6 +626,11 @@ using namespace ntp;
 extern "C" {
 
 int ntp_set_option(int option, int64_t value) {
+  if (option == NTP_OPT_SYNC_MAX_CTAS) {
+    if (value < 0 || value > 1 << 20) return fail(NTP_EINVAL, "bad CTA cap");
+    g_max_ctas.store((int)value);
+    return NTP_OK;
+  }
   if (option != NTP_OPT_SYNC_KERNEL) return fail(NTP_EINVAL, "unknown option");
   if (value < NTP_KERNEL_AUTO || value > NTP_KERNEL_BULK2)
     return fail(NTP_EINVAL, "unknown sync kernel variant");
@@ -626,6 +639,7 @@ int ntp_set_option(int option, int64_t value) {
 }
 
 int64_t ntp_get_option(int option) {
+  if (option == NTP_OPT_SYNC_MAX_CTAS) return g_max_ctas.load();
   if (option != NTP_OPT_SYNC_KERNEL) return fail(NTP_EINVAL, "unknown option");
   return g_sync_kernel.load();
 }

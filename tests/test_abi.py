@@ -109,3 +109,12 @@ def test_plan_state_errors():
         p.add_units(4, [0], [4], [1], [4])
     with pytest.raises(ValueError):
         Plan(_lib.NTP_F32).add_units(4, [70], [0], [1], [0])
+
+
+def test_options_round_trip():
+    L = _lib.load()
+    assert L.ntp_get_option(0) == 0  # AUTO sync-kernel selection by default
+    assert L.ntp_set_option(1, 24) == 0 and L.ntp_get_option(1) == 24
+    assert L.ntp_set_option(1, 0) == 0 and L.ntp_get_option(1) == 0
+    assert L.ntp_set_option(0, 9) == _lib.NTP_EINVAL
+    assert L.ntp_set_option(7, 1) == _lib.NTP_EINVAL
