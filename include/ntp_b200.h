@@ -226,6 +226,11 @@ int ntp_gemm_bf16(const void *A, int64_t lda, int a_mn, const void *B, int64_t l
  * cluster of 2); 0: 128 x 256 tiles on single CTAs. */
 int ntp_gemm_set_pair(int on);
 
+/* Cap on the persistent GEMM's CTAs (0 = every SM).  With a sync kernel capped
+ * to c CTAs (NTP_OPT_SYNC_MAX_CTAS), a GEMM cap of SMs - c lets the two run
+ * side by side when the sync overlaps the backward pass. */
+int ntp_gemm_set_max_ctas(int n);
+
 /* ------------------------------------------------------------------------
  * Multi-GPU plumbing: peer memory over NVLink/NVSwitch and device signals
  * ------------------------------------------------------------------------ */

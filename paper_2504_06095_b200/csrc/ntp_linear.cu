@@ -544,6 +544,9 @@ static int sm_count_dev() {
   return cache[dev & 63];
 }
 
+static std::atomic<int> g_pair{1};
+static std::atomic<int> g_max_ctas{0};
+
 template <int BN, int kPair, int kStg>
 static int launch(const void *A, long long lda, int a_mn, const void *B, long long ldb, int b_mn,
                   void *C, long long ldc, void *H, long long ldh, Params p, cudaStream_t s) {
@@ -584,7 +587,10 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
   p.num_m = (p.M + BM * kPair - 1) / (BM * kPair);
   p.num_n = (p.N + BN - 1) / BN;
   const int tiles = p.num_m * p.num_n;
-  const int units = sm_count_dev() / kPair;
+  int sms = sm_count_dev();
+  const int cap = g_max_ctas.load();
+  if (cap > 0 && cap < sms) sms = cap;  // leave SMs to a concurrent sync kernel
+  const int units = sms / kPair > 0 ? sms / kPair : 1;
   const int grid = (tiles < units ? tiles : units) * kPair;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -604,7 +610,6 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
   return NTP_OK;
 }
 
-static std::atomic<int> g_pair{1};
 
 }  // namespace gemm
 }  // namespace ntp
@@ -635,6 +640,13 @@ extern "C" int ntp_gemm_bf16(const void *A, int64_t lda, int a_mn, const void *B
 }
 
 // 1 (default): 256-row CTA-pair tiles (tcgen05 cta_group::2) for N > 128; 0: 1-SM tiles.
+// Cap on persistent GEMM CTAs (0 = all SMs): overlap with a CTA-capped sync.
+extern "C" int ntp_gemm_set_max_ctas(int n) {
+  if (n < 0) return fail(NTP_EINVAL, "bad CTA cap");
+  gemm::g_max_ctas.store(n);
+  return NTP_OK;
+}
+
 extern "C" int ntp_gemm_set_pair(int on) {
   gemm::g_pair.store(on ? 1 : 0);
   return NTP_OK;

@@ -78,7 +78,7 @@ def run_config(args, n1, n2, local):
     torch.cuda.synchronize()
     dist.barrier()
     main = torch.cuda.current_stream()
-    side = torch.cuda.Stream()
+    side = torch.cuda.Stream(priority=-1)  # sync CTAs are scheduled ahead of GEMM CTAs
 
     def backward(overlap: bool, sync: bool = True):
         for li in reversed(range(L)):
@@ -119,10 +119,20 @@ def run_config(args, n1, n2, local):
     res["backward_ms"] = round(timed(lambda: backward(False, sync=False), args.iters), 3)
     res["sync_ms"] = round(timed(sync_only, args.iters), 3)
     res["serial_ms"] = round(timed(lambda: backward(False), args.iters), 3)
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
     for cap in args.caps:
+        # the sync gets `cap` CTAs, the persistent GEMMs the remaining SMs
         Lb.ntp_set_option(1, cap)
+        Lb.ntp_gemm_set_max_ctas(sms - cap if cap else 0)
         res[f"overlap_ms_cap{cap}"] = round(timed(lambda: backward(True), args.iters), 3)
     Lb.ntp_set_option(1, 0)
+    Lb.ntp_gemm_set_max_ctas(0)
+    if args.caps:
+        # backward alone on the reduced SM count, for reference
+        Lb.ntp_gemm_set_max_ctas(sms - max(args.caps))
+        res[f"backward_ms_gemm_cap{sms - max(args.caps)}"] = round(
+            timed(lambda: backward(False, sync=False), args.iters), 3)
+        Lb.ntp_gemm_set_max_ctas(0)
     for gr in groups:
         assert gr.status() == 0, "signal timeout"
         gr.close()
@@ -136,7 +146,7 @@ def main():
     ap.add_argument("--hidden", type=int, default=4096)
     ap.add_argument("--ffn", type=int, default=14336)
     ap.add_argument("--iters", type=int, default=5)
-    ap.add_argument("--caps", type=int, nargs="*", default=[16, 32, 0])
+    ap.add_argument("--caps", type=int, nargs="*", default=[8, 16, 24, 0])
     args = ap.parse_args()
     os.environ["NCCL_DEBUG"] = "WARN"
     local = int(os.environ["LOCAL_RANK"])
