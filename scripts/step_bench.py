@@ -121,18 +121,21 @@ def run_config(args, n1, n2, local):
     res["serial_ms"] = round(timed(lambda: backward(False), args.iters), 3)
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     for cap in args.caps:
-        # the sync gets `cap` CTAs, the persistent GEMMs the remaining SMs
+        # TMA-bulk sync (131 KB smem/CTA): it cannot share an SM with a GEMM CTA,
+        # so the sync gets `cap` SMs and the persistent GEMMs the remaining ones
+        Lb.ntp_set_option(0, 2)
         Lb.ntp_set_option(1, cap)
         Lb.ntp_gemm_set_max_ctas(sms - cap if cap else 0)
-        res[f"overlap_ms_cap{cap}"] = round(timed(lambda: backward(True), args.iters), 3)
-    Lb.ntp_set_option(1, 0)
+        res[f"overlap_ms_bulk_cap{cap}"] = round(timed(lambda: backward(True), args.iters), 3)
     Lb.ntp_gemm_set_max_ctas(0)
-    if args.caps:
-        # backward alone on the reduced SM count, for reference
-        Lb.ntp_gemm_set_max_ctas(sms - max(args.caps))
-        res[f"backward_ms_gemm_cap{sms - max(args.caps)}"] = round(
-            timed(lambda: backward(False, sync=False), args.iters), 3)
-        Lb.ntp_gemm_set_max_ctas(0)
+    for cap in args.ldg_caps:
+        # register-staged sync (no smem): its CTAs co-reside with the GEMM's
+        # 1 CTA/SM, so the GEMMs keep every SM
+        Lb.ntp_set_option(0, 1)
+        Lb.ntp_set_option(1, cap)
+        res[f"overlap_ms_ldg_cap{cap}"] = round(timed(lambda: backward(True), args.iters), 3)
+    Lb.ntp_set_option(0, 0)
+    Lb.ntp_set_option(1, 0)
     for gr in groups:
         assert gr.status() == 0, "signal timeout"
         gr.close()
@@ -146,7 +149,8 @@ def main():
     ap.add_argument("--hidden", type=int, default=4096)
     ap.add_argument("--ffn", type=int, default=14336)
     ap.add_argument("--iters", type=int, default=5)
-    ap.add_argument("--caps", type=int, nargs="*", default=[8, 16, 24, 0])
+    ap.add_argument("--caps", type=int, nargs="*", default=[16])
+    ap.add_argument("--ldg-caps", type=int, nargs="*", default=[32, 74, 148, 296])
     args = ap.parse_args()
     os.environ["NCCL_DEBUG"] = "WARN"
     local = int(os.environ["LOCAL_RANK"])
