@@ -631,12 +631,26 @@ extern "C" int ntp_gemm_bf16(const void *A, int64_t lda, int a_mn, const void *B
                  nullptr, nullptr, 0, 0, 0, 0};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   void *H = const_cast<void *>(aux);
-  if (N > 128) {
-    if (gemm::g_pair.load())
-      return gemm::launch<256, 2, 6>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
-    return gemm::launch<256, 1, 4>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
+  if (!gemm::g_pair.load()) {
+    if (N > 128) return gemm::launch<256, 1, 4>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
+    return gemm::launch<128, 1, 4>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
   }
-  return gemm::launch<128, 1, 4>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
+  // CTA-pair tiles 256 x 256 or 256 x 128: pick the one with the fewer per-SM
+  // MACs over the whole (wave-quantized) persistent schedule -- a ragged tile
+  // count that spills a few tiles into an extra wave costs a full wave.
+  int sms = gemm::sm_count_dev();
+  const int cap = gemm::g_max_ctas.load();
+  if (cap > 0 && cap < sms) sms = cap;
+  const long long pairs = sms / 2 > 0 ? sms / 2 : 1;
+  auto cost = [&](long long bn) {
+    const long long tiles = ((M + 255) / 256) * ((N + bn - 1) / bn);
+    return ((tiles + pairs - 1) / pairs) * bn;  // rounds x per-SM tile width
+  };
+  const int mode = gemm::g_pair.load();
+  const bool wide = mode == 3 || (mode == 1 && cost(256) * 10 <= cost(128) * 11);
+  if (N > 128 && mode != 2 && wide)
+    return gemm::launch<256, 2, 6>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
+  return gemm::launch<128, 2, 8>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
 }
 
 // 1 (default): 256-row CTA-pair tiles (tcgen05 cta_group::2) for N > 128; 0: 1-SM tiles.
@@ -647,7 +661,8 @@ extern "C" int ntp_gemm_set_max_ctas(int n) {
   return NTP_OK;
 }
 
-extern "C" int ntp_gemm_set_pair(int on) {
-  gemm::g_pair.store(on ? 1 : 0);
+extern "C" int ntp_gemm_set_pair(int mode) {
+  if (mode < 0 || mode > 3) return fail(NTP_EINVAL, "pair mode must be 0..3");
+  gemm::g_pair.store(mode);
   return NTP_OK;
 }

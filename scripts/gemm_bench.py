@@ -60,15 +60,19 @@ def main():
         from paper_2504_06095_b200 import _lib
         for name, ours, ref, M, N, K in cases:
             fl = 2.0 * M * N * K
-            _lib.load().ntp_gemm_set_pair(0)
-            ms1 = timed(ours)
-            _lib.load().ntp_gemm_set_pair(1)
-            ms = timed(ours)
+            modes = {}
+            for mode, name_m in ((0, "single_256"), (2, "pair_128"), (3, "pair_256"), (1, "auto")):
+                _lib.load().ntp_gemm_set_pair(mode)
+                modes[name_m] = timed(ours)
+            ms1 = modes["single_256"]
+            ms = modes["auto"]
             ms_ref = timed(ref)
             out["gemms"].append({"n_i": n, "gemm": name, "M": M, "N": N, "K": K,
                                  "ours_ms": round(ms, 4), "ours_tflops": round(fl / ms / 1e9, 1),
                                  "ours_frac": round(fl / ms / 1e9 / PEAK, 3),
                                  "single_cta_tflops": round(fl / ms1 / 1e9, 1),
+                                 "tflops_by_tile": {k: round(fl / v / 1e9, 1)
+                                                    for k, v in modes.items()},
                                  "cublas_ms": round(ms_ref, 4),
                                  "cublas_tflops": round(fl / ms_ref / 1e9, 1)})
     print(json.dumps(out, indent=1))

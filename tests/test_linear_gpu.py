@@ -14,13 +14,13 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module", params=[1, 0], ids=["pair", "single"])
+@pytest.fixture(scope="module", params=[3, 2, 0], ids=["pair256", "pair128", "single"])
 def Lin(request):
     """Both tile paths: CTA pairs (tcgen05 cta_group::2) and single CTAs."""
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
     from paper_2504_06095_b200 import _lib, linear
-    _lib.load().ntp_gemm_set_pair(request.param)
+    _lib.load().ntp_gemm_set_pair(request.param)  # 1 auto (pair tiles), 0 single-CTA
     yield linear
     _lib.load().ntp_gemm_set_pair(1)
 
