@@ -175,3 +175,23 @@ def test_single_process_emulation_of_larger_worlds(world, n1, n2):
         tab = np.array(rows, dtype=np.int64).reshape(-1, 5)
         per_rank[rank] = (tab, list(range(n1 + n2)))
     _replay(lay, per_rank)
+
+
+def test_gloo_world8_tp4_tp3_plans_and_wiring():
+    """The 8-GPU bench placement: TP4 + TP3 on 7 ranks, rank 7 idle ("failed")."""
+    per_rank = _run_world(8, 4, 3)
+    lay = pair_layout(SHAPE, 4, 3)
+    _replay(lay, per_rank)
+    _check_wiring(per_rank)
+    assert len(per_rank[7][0]) == 0 and per_rank[7][6] == []  # idle GPU: no work, no partners
+
+
+def test_busiest_bytes_accounting():
+    from paper_2504_06095_b200.dist_bench import busiest_bytes_for
+    from paper_2504_06095_b200.workloads import GPT_1_3B
+    lay = pair_layout(GPT_1_3B, 4, 3)
+    # 8 GPUs: the busiest reduced GPU owns sync shard 0 (2731 MLP cols + 6 heads per layer)
+    b8 = busiest_bytes_for(lay, D.Placement.default(8, 4, 3), 2)
+    assert b8 == max(lay.r_elems) * 2 == 838926336
+    # 2 GPUs: every unit crosses the one link
+    assert busiest_bytes_for(lay, D.Placement.default(2, 4, 3), 2) == lay.elems * 2
