@@ -647,7 +647,11 @@ extern "C" int ntp_gemm_bf16(const void *A, int64_t lda, int a_mn, const void *B
     return ((tiles + pairs - 1) / pairs) * bn;  // rounds x per-SM tile width
   };
   const int mode = gemm::g_pair.load();
-  const bool wide = mode == 3 || (mode == 1 && cost(256) * 10 <= cost(128) * 11);
+  // Measured (profiles/r01_gemm_bench_v5.json): 256-wide pair tiles beat 128-wide
+  // ones by 1.3-1.6x on every C4 GEMM even where they lose a wave to quantization
+  // (the narrow tile doubles the A-operand bytes per MAC), so AUTO only takes
+  // the narrow tile when the wide one would need twice the waves.
+  const bool wide = mode == 3 || (mode == 1 && cost(256) <= 2 * cost(128));
   if (N > 128 && mode != 2 && wide)
     return gemm::launch<256, 2, 6>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
   return gemm::launch<128, 2, 8>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
