@@ -302,9 +302,13 @@ class NtpSyncGroup:
         return int(self._status.item()) if self._status is not None else 0
 
     def close(self) -> None:
+        """Collective: unmap peers' memory, wait until every process has, then free ours."""
+        if torch.cuda.is_available():
+            torch.cuda.synchronize(self.device)
         for p in list(self.opened.values()) + list(self.peer_sig.values()):
             self.ops.close(p)
         self.opened, self.peer_sig = {}, {}
+        dist.barrier()
         for p in self.local.values():
             self.ops.free(p)
         self.ops.free(self.sig)

@@ -216,8 +216,11 @@ class NtpDpGroup:
         return int(self._status.item()) if self._status is not None else 0
 
     def close(self) -> None:
+        """Collective: unmap peers' memory, wait until every process has, then free ours."""
+        torch.cuda.synchronize(self.device)
         for p in list(self.opened.values()) + list(self.peer_sig.values()):
             self.ops.close(p)
+        dist.barrier()
         for p in self.local.values():
             self.ops.free(p)
         self.ops.free(self.sig)
