@@ -36,7 +36,9 @@ def run(args):
     if not dist.is_initialized():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, world = dist.get_rank(), dist.get_world_size()
-    _lib.load()
+    L = _lib.load()
+    if os.environ.get("NTP_SYNC_KERNEL"):  # experiments: 1 LDG, 2 BULK, 3 BULK2
+        _lib.check(L.ntp_set_option(0, int(os.environ["NTP_SYNC_KERNEL"])))
     shape = SHAPES[args.workload]
     n1, n2 = 4, 3
     lay = pair_layout(shape, n1, n2)
