@@ -222,9 +222,24 @@ int ntp_gemm_bf16(const void *A, int64_t lda, int a_mn, const void *B, int64_t l
                   void *C, int64_t ldc, int c_f32, int64_t M, int64_t N, int64_t K, int epilogue,
                   const void *aux, int64_t ld_aux, float alpha, void *stream);
 
-/* 1 (default): N > 128 uses 256 x 256 tiles on CTA pairs (tcgen05.mma.cta_group::2,
- * cluster of 2); 0: 128 x 256 tiles on single CTAs. */
-int ntp_gemm_set_pair(int on);
+/* Fused weight-gradient GEMM + NTP gradient sync: the epilogue adds
+ * alpha * acc (this replica's batch-weighted gradient) with red.add into the
+ * local row m of C AND into row red_row[m] of the partner replica's copy
+ * red_base[red_buf[m]] (local or peer-mapped; red_buf[m] < 0: no partner).
+ * Both copies must start at zero; since each unit receives exactly two
+ * contributions and a two-term floating-point sum commutes, both replicas end
+ * with identical bits -- nonuniform_grad_sync (tpnumerics.py:289-356) done
+ * inside the producer of the gradients, with no separate sync kernel.
+ * red_buf/red_row are device int32[M]; N % 32 == 0; 16-byte aligned rows. */
+int ntp_gemm_bf16_red(const void *A, int64_t lda, int a_mn, const void *B, int64_t ldb, int b_mn,
+                      void *C, int64_t ldc, int c_f32, int64_t M, int64_t N, int64_t K,
+                      float alpha, const int32_t *red_buf, const int32_t *red_row,
+                      void *const *red_base, int n_red, int64_t red_ld, void *stream);
+
+/* Tile selection: 1 (default) AUTO -- 256 x 256 CTA-pair tiles (tcgen05
+ * cta_group::2, cluster of 2) unless 256 x 128 pair tiles halve the waves;
+ * 2 force 256 x 128 pair tiles; 3 force 256 x 256; 0 single-CTA 128 x 256. */
+int ntp_gemm_set_pair(int mode);
 
 /* Cap on the persistent GEMM's CTAs (0 = every SM).  With a sync kernel capped
  * to c CTAs (NTP_OPT_SYNC_MAX_CTAS), a GEMM cap of SMs - c lets the two run

@@ -39,7 +39,9 @@ constexpr int kStages = 4;
 constexpr int kThreads = 192;   // 6 warps
 constexpr int kEpiWarp0 = 2;
 
-enum Epi { EPI_NONE = 0, EPI_GELU = 1, EPI_DGELU = 2 };
+enum Epi { EPI_NONE = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_RED = 3 };
+
+constexpr int kMaxPeers = 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -148,7 +150,39 @@ struct Params {
   void *C, *H;             // outputs (H: EPI_GELU pre-activation)
   long long ldc, ldh;
   int c_tma, h_tma;        // 1: 16-byte aligned pitch -> TMA store; 0: warp copy
+  // EPI_RED (fused wgrad + NTP sync): row m of the tile is added (red.add) to
+  // the local C row and to row red_row[m] of peer copy red_buf[m] (-1: none)
+  const int *red_buf;
+  const int *red_row;
+  char *red_base[kMaxPeers];
+  long long red_ld;        // elements
 };
+
+// red.add of 32 consecutive values (fp32 or bf16 destination, 16-byte aligned)
+__device__ __forceinline__ void red_row32(void *dst, const float *f, int c_f32) {
+  if (c_f32) {
+    float *d = reinterpret_cast<float *>(dst);
+#pragma unroll
+    for (int j = 0; j < 32; j += 4)
+      asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d + j), "f"(f[j]),
+                   "f"(f[j + 1]), "f"(f[j + 2]), "f"(f[j + 3])
+                   : "memory");
+  } else {
+    __nv_bfloat16 *d = reinterpret_cast<__nv_bfloat16 *>(dst);
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        __nv_bfloat162 t = __floats2bfloat162_rn(f[j + 2 * e], f[j + 2 * e + 1]);
+        w[e] = *reinterpret_cast<uint32_t *>(&t);
+      }
+      asm volatile("red.global.add.noftz.v4.bf16x2 [%0], {%1, %2, %3, %4};" ::"l"(d + j),
+                   "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                   : "memory");
+    }
+  }
+}
 
 // Copy a staged 32 x 32 box to global with row/column masking (pitches a TMA
 // map cannot describe).  esize = 2 (bf16) or 4 (fp32).
@@ -399,6 +433,21 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         float f[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]) * p.alpha;
+        if (p.epi == EPI_RED) {
+          // fused sync: this replica's weighted contribution is added into its own
+          // copy and into the partner replica's copy of the same unit (peer HBM
+          // over NVLink); both copies start at zero, and two-term fp additions
+          // commute, so both replicas end with identical bits.
+          if (row < p.M && col0 + 32 <= p.N) {
+            const int ce = p.c_f32 ? 4 : 2;
+            red_row32(static_cast<char *>(p.C) + ((long long)row * p.ldc + col0) * ce, f, p.c_f32);
+            const int pb = p.red_buf[row];
+            if (pb >= 0)
+              red_row32(p.red_base[pb] + ((long long)p.red_row[row] * p.red_ld + col0) * ce, f,
+                        p.c_f32);
+          }
+          continue;
+        }
         // the previous TMA store of this warp must have finished reading `stage`
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
@@ -567,7 +616,7 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
   p.H = H;
   p.ldc = ldc;
   p.ldh = ldh;
-  p.c_tma = !((reinterpret_cast<uintptr_t>(C) & 15u) || ((ldc * ce) & 15));
+  p.c_tma = p.epi != EPI_RED && !((reinterpret_cast<uintptr_t>(C) & 15u) || ((ldc * ce) & 15));
   p.h_tma = p.epi == EPI_GELU && !((reinterpret_cast<uintptr_t>(H) & 15u) || ((ldh * 2) & 15));
   memset(&mc, 0, sizeof mc);
   memset(&mh, 0, sizeof mh);
@@ -614,6 +663,13 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
 }  // namespace gemm
 }  // namespace ntp
 
+namespace ntp {
+namespace gemm {
+int dispatch(const void *A, long long lda, int a_mn, const void *B, long long ldb, int b_mn,
+             void *C, long long ldc, void *H, long long ld_aux, Params p, cudaStream_t s);
+}  // namespace gemm
+}  // namespace ntp
+
 using namespace ntp;
 
 extern "C" int ntp_gemm_bf16(const void *A, int64_t lda, int a_mn, const void *B, int64_t ldb,
@@ -629,8 +685,43 @@ extern "C" int ntp_gemm_bf16(const void *A, int64_t lda, int a_mn, const void *B
   gemm::Params p{(int)M, (int)N, (int)K, a_mn ? 1 : 0, b_mn ? 1 : 0, c_f32 ? 1 : 0, epilogue,
                  static_cast<const __nv_bfloat16 *>(aux), ld_aux, alpha, 0, 0,
                  nullptr, nullptr, 0, 0, 0, 0};
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  void *H = const_cast<void *>(aux);
+  return gemm::dispatch(A, lda, a_mn, B, ldb, b_mn, C, ldc, const_cast<void *>(aux), ld_aux, p,
+                        static_cast<cudaStream_t>(stream));
+}
+
+// Fused weight-gradient GEMM + NTP gradient sync (EPI_RED, see the epilogue).
+extern "C" int ntp_gemm_bf16_red(const void *A, int64_t lda, int a_mn, const void *B,
+                                 int64_t ldb, int b_mn, void *C, int64_t ldc, int c_f32,
+                                 int64_t M, int64_t N, int64_t K, float alpha,
+                                 const int32_t *red_buf, const int32_t *red_row,
+                                 void *const *red_base, int n_red, int64_t red_ld,
+                                 void *stream) {
+  if (M <= 0 || N <= 0 || K <= 0) return fail(NTP_EINVAL, "GEMM extents must be positive");
+  if (N % 32) return fail(NTP_EINVAL, "fused sync GEMM needs N % 32 == 0");
+  if (n_red < 0 || n_red > gemm::kMaxPeers) return fail(NTP_EINVAL, "at most 8 peer copies");
+  if (!red_buf || !red_row) return fail(NTP_EINVAL, "fused sync GEMM needs a row map");
+  const int ce = c_f32 ? 4 : 2;
+  if ((reinterpret_cast<uintptr_t>(C) & 15u) || ((ldc * ce) & 15) || ((red_ld * ce) & 15))
+    return fail(NTP_EINVAL, "fused sync GEMM needs 16-byte aligned rows");
+  gemm::Params p{(int)M, (int)N, (int)K, a_mn ? 1 : 0, b_mn ? 1 : 0, c_f32 ? 1 : 0,
+                 gemm::EPI_RED, nullptr, 0, alpha, 0, 0, nullptr, nullptr, 0, 0, 0, 0};
+  p.red_buf = red_buf;
+  p.red_row = red_row;
+  for (int i = 0; i < gemm::kMaxPeers; ++i)
+    p.red_base[i] = i < n_red ? static_cast<char *>(red_base[i]) : nullptr;
+  for (int i = 0; i < n_red; ++i)
+    if (reinterpret_cast<uintptr_t>(p.red_base[i]) & 15u)
+      return fail(NTP_EINVAL, "peer copies must be 16-byte aligned");
+  p.red_ld = red_ld;
+  return gemm::dispatch(A, lda, a_mn, B, ldb, b_mn, C, ldc, nullptr, 0, p,
+                        static_cast<cudaStream_t>(stream));
+}
+
+namespace ntp {
+namespace gemm {
+int dispatch(const void *A, long long lda, int a_mn, const void *B, long long ldb, int b_mn,
+             void *C, long long ldc, void *H, long long ld_aux, Params p, cudaStream_t s) {
+  const long long M = p.M, N = p.N;
   if (!gemm::g_pair.load()) {
     if (N > 128) return gemm::launch<256, 1, 4>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
     return gemm::launch<128, 1, 4>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
@@ -656,6 +747,8 @@ extern "C" int ntp_gemm_bf16(const void *A, int64_t lda, int a_mn, const void *B
     return gemm::launch<256, 2, 6>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
   return gemm::launch<128, 2, 8>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
 }
+}  // namespace gemm
+}  // namespace ntp
 
 // 1 (default): 256-row CTA-pair tiles (tcgen05 cta_group::2) for N > 128; 0: 1-SM tiles.
 // Cap on persistent GEMM CTAs (0 = all SMs): overlap with a CTA-capped sync.

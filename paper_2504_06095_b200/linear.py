@@ -72,6 +72,43 @@ def mm(A: torch.Tensor, Bt: torch.Tensor, out: torch.Tensor, *, epilogue: str = 
     return out
 
 
+def mm_red(A: torch.Tensor, Bt: torch.Tensor, out: torch.Tensor, alpha: float,
+           red_buf: torch.Tensor, red_row: torch.Tensor, red_bases, red_ld: int,
+           stream=None) -> None:
+    """Fused wgrad + sync: red.add(alpha * A @ Bt^T) into ``out`` (local copy) and
+    into row red_row[m] of red_bases[red_buf[m]] (the partner's copy); both must
+    start at zero.  red_buf/red_row: int32 device tensors [M]."""
+    M, K = A.shape
+    N, K2 = Bt.shape
+    if K != K2 or tuple(out.shape) != (M, N) or out.stride(1) != 1:
+        raise ValueError("shape mismatch")
+    if red_buf.dtype != torch.int32 or red_row.dtype != torch.int32 or len(red_buf) != M:
+        raise ValueError("red_buf/red_row must be int32 [M]")
+    a_ptr, lda, a_mn = _operand(A)
+    b_ptr, ldb, b_mn = _operand(Bt)
+    if stream is None:
+        stream = torch.cuda.current_stream(A.device)
+    _lib.check(_lib.load().ntp_gemm_bf16_red(
+        ctypes.c_void_p(a_ptr), lda, a_mn, ctypes.c_void_p(b_ptr), ldb, b_mn,
+        ctypes.c_void_p(out.data_ptr()), out.stride(0), int(out.dtype == torch.float32),
+        M, N, K, float(alpha), ctypes.c_void_p(red_buf.data_ptr()),
+        ctypes.c_void_p(red_row.data_ptr()), _lib.ptr_array(red_bases), len(red_bases),
+        int(red_ld), ctypes.c_void_p(stream.cuda_stream)), "ntp_gemm_bf16_red")
+
+
+def partner_row_map(cols, partner_cols, device):
+    """For a shard whose rows are units `cols`, the (buffer, row) of each unit in
+    the partner replica's per-rank layout `partner_cols` (list of arrays)."""
+    k = int(max(max(c.max() for c in partner_cols if len(c)), np.max(cols))) + 1
+    owner = np.full(k, -1, dtype=np.int32)
+    pos = np.zeros(k, dtype=np.int32)
+    for r, c in enumerate(partner_cols):
+        owner[c] = r
+        pos[c] = np.arange(len(c), dtype=np.int32)
+    cols = np.asarray(cols)
+    return (torch.from_numpy(owner[cols]).to(device), torch.from_numpy(pos[cols]).to(device))
+
+
 def _pad8(n: int) -> int:
     return (n + 7) // 8 * 8
 
@@ -115,6 +152,25 @@ class MlpShard:
         mm(G, self.W[:, 1, :], D, epilogue="dgelu", aux=H)
         mm(Y.T, G.T, grads[:, 1, :])
         mm(D.T, X.T, grads[:, 0, :])
+
+    def backward_synced(self, X: torch.Tensor, G: torch.Tensor, grads: torch.Tensor, alpha: float,
+                        red_buf: torch.Tensor, red_row: torch.Tensor, partner_arenas,
+                        stream=None) -> None:
+        """backward() with the NTP sync fused into the weight-gradient epilogues:
+        alpha * dB, alpha * dA^T are red.add-ed into this rank's unit-major arena
+        and into the partner replica's arenas (zeroed beforehand).  After both
+        replicas' fused backward the arenas hold w_h*g_h + w_r*g_r."""
+        T = X.shape[0]
+        H, Y = self.H[:, :self.n], self.Y[:, :self.n]
+        Dfull = torch.empty((T, _pad8(self.n)), dtype=torch.bfloat16, device=X.device)
+        D = Dfull[:, :self.n]
+        mm(G, self.W[:, 1, :], D, epilogue="dgelu", aux=H, stream=stream)
+        eb = grads.element_size()
+        h = self.h
+        bases_b = [int(t.data_ptr()) + h * eb for t in partner_arenas]
+        bases_a = [int(t.data_ptr()) for t in partner_arenas]
+        mm_red(Y.T, G.T, grads[:, 1, :], alpha, red_buf, red_row, bases_b, 2 * h, stream)
+        mm_red(D.T, X.T, grads[:, 0, :], alpha, red_buf, red_row, bases_a, 2 * h, stream)
 
 
 def mlp_forward_tp(X: torch.Tensor, shards) -> torch.Tensor:
