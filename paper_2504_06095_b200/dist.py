@@ -298,6 +298,35 @@ class NtpSyncGroup:
             _lib.check(L.ntp_signal_wait(_lib.u64_ptr_array(self.wait_done), len(self.wait_done),
                                          e, spin_ns, st, sp), "ntp_signal_wait")
 
+    def open_slots(self, slots) -> list:
+        """Device pointers of the given logical slots (IPC-mapping peers' arenas
+        on first use): the partner copies a fused wgrad+sync GEMM reduces into."""
+        out = []
+        for s in slots:
+            if s not in self.slot_ptr:
+                proc = self.plc.proc_of_slot(s)
+                self.slot_ptr[s] = self.opened[s] = self.ops.open(self.table[proc]["slots"][s])
+            out.append(self.slot_ptr[s])
+        return out
+
+    def signal(self, kind: str, epoch: int, stream=None, spin_ns: int = 20_000_000_000) -> None:
+        """Stream-ordered handshake with every partner: kind = "post_ready",
+        "wait_ready", "post_done" or "wait_done" (the words step() uses)."""
+        if not self.partners:
+            return
+        L = _lib.load()
+        s = torch.cuda.current_stream(self.device) if stream is None else stream
+        sp = ctypes.c_void_p(s.cuda_stream)
+        words = {"post_ready": self.post_ready, "wait_ready": self.wait_ready,
+                 "post_done": self.post_done, "wait_done": self.wait_done}[kind]
+        arr = _lib.u64_ptr_array(words)
+        if kind.startswith("post"):
+            _lib.check(L.ntp_signal_post(arr, len(words), int(epoch), sp), "ntp_signal_post")
+        else:
+            st = ctypes.cast(self._status.data_ptr(), ctypes.POINTER(ctypes.c_int))
+            _lib.check(L.ntp_signal_wait(arr, len(words), int(epoch), spin_ns, st, sp),
+                       "ntp_signal_wait")
+
     def status(self) -> int:
         return int(self._status.item()) if self._status is not None else 0
 

@@ -98,6 +98,44 @@ def run_config(args, n1, n2, local):
         for li in reversed(range(L)):
             groups[li].step(w_h, w_r, main)
 
+    # fused wgrad + sync: every GPU's wgrad epilogue red.adds its weighted
+    # gradient into its own arena and the partner replica's (zeroed first)
+    from paper_2504_06095_b200.linear import partner_row_map
+    fused = []
+    for li in range(L):
+        per = []
+        for (sh, X, G, grads), s in zip(shards[li], groups[li].hosted):
+            healthy = s < n1
+            cols = hc[s] if healthy else rc[s - n1]
+            partner_cols = rc if healthy else hc
+            partner_slots = [n1 + j for j in range(n2)] if healthy else list(range(n1))
+            ptrs = groups[li].open_slots(partner_slots)
+            rb, rr = partner_row_map(cols, partner_cols, "cuda")
+            per.append((sh, X, G, grads, w_h if healthy else w_r, rb, rr, ptrs))
+        fused.append(per)
+
+    class _P:  # raw pointer holder with the .data_ptr() mm_red expects
+        def __init__(self, p):
+            self.p = p
+
+        def data_ptr(self):
+            return self.p
+
+    def fused_backward():
+        for li in range(L):
+            gr = groups[li]
+            gr.epoch += 1
+            for s in gr.hosted:
+                gr.arena(s).zero_()
+            gr.signal("post_ready", gr.epoch, main)
+            gr.signal("wait_ready", gr.epoch, main)
+        for li in reversed(range(L)):
+            for sh, X, G, grads, alpha, rb, rr, ptrs in fused[li]:
+                sh.backward_synced(X, G, grads, alpha, rb, rr, [_P(p) for p in ptrs], main)
+            groups[li].signal("post_done", groups[li].epoch, main)
+        for li in range(L):
+            groups[li].signal("wait_done", groups[li].epoch, main)
+
     def timed(fn, iters):
         for _ in range(2):
             fn()
@@ -119,6 +157,7 @@ def run_config(args, n1, n2, local):
     res["backward_ms"] = round(timed(lambda: backward(False, sync=False), args.iters), 3)
     res["sync_ms"] = round(timed(sync_only, args.iters), 3)
     res["serial_ms"] = round(timed(lambda: backward(False), args.iters), 3)
+    res["fused_wgrad_sync_ms"] = round(timed(fused_backward, args.iters), 3)
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     for cap in args.caps:
         # TMA-bulk sync (131 KB smem/CTA): it cannot share an SM with a GEMM CTA,
@@ -161,7 +200,8 @@ def main():
     ntp = run_config(args, n1, n1 - 1, local) if n1 > 1 else None
     uni = run_config(args, n1, n1, local)
     if dist.get_rank() == 0:
-        best = lambda r: min(v for key, v in r.items() if key.startswith("overlap_ms"))  # noqa: E731
+        best = lambda r: min(v for key, v in r.items()  # noqa: E731
+                             if key.startswith("overlap_ms") or key.startswith("fused"))
         doc = {"world": world, "layers": args.layers, "hidden": args.hidden, "ffn": args.ffn,
                "ntp": ntp, "uniform": uni}
         if ntp:
