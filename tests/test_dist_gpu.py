@@ -60,3 +60,9 @@ def test_four_gpus_dp3_with_degraded_replica(dtype):
 def test_eight_gpus_c3():
     """BASELINE configs[2]: DP=4 x TP2 with one replica degraded to TP1 (7 GPUs)."""
     _run_script(8, "dp_check.py", 3, 2, 1, "bf16", 2)
+
+
+@pytest.mark.parametrize("n,n1,n2", [(2, 2, 1), (4, 2, 1)])
+def test_fused_wgrad_sync_multi_gpu(n, n1, n2):
+    """tcgen05 wgrad epilogues red.add into the partner replica over NVLink."""
+    _run_script(n, "fused_check.py", n1, n2)
