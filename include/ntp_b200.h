@@ -230,11 +230,15 @@ int ntp_gemm_bf16(const void *A, int64_t lda, int a_mn, const void *B, int64_t l
  * contributions and a two-term floating-point sum commutes, both replicas end
  * with identical bits -- nonuniform_grad_sync (tpnumerics.py:289-356) done
  * inside the producer of the gradients, with no separate sync kernel.
- * red_buf/red_row are device int32[M]; N % 32 == 0; 16-byte aligned rows. */
+ * red_buf/red_row are device int32[M]; N % 32 == 0; 16-byte aligned rows.
+ * mode 0: red.add into zeroed arenas as above.  mode 1 (push): plain stores of
+ * the weighted tile into the local arena and into the partner's *staging*
+ * arena (red_base); after the done handshake each side adds its staging into
+ * its arena (ntp_grad_sync_ex with write mask 1) -- no remote atomics. */
 int ntp_gemm_bf16_red(const void *A, int64_t lda, int a_mn, const void *B, int64_t ldb, int b_mn,
                       void *C, int64_t ldc, int c_f32, int64_t M, int64_t N, int64_t K,
                       float alpha, const int32_t *red_buf, const int32_t *red_row,
-                      void *const *red_base, int n_red, int64_t red_ld, void *stream);
+                      void *const *red_base, int n_red, int64_t red_ld, int mode, void *stream);
 
 /* Tile selection: 1 (default) AUTO -- 256 x 256 CTA-pair tiles (tcgen05
  * cta_group::2, cluster of 2) unless 256 x 128 pair tiles halve the waves;

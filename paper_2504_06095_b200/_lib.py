@@ -82,7 +82,7 @@ SIGNATURES = {
                                          ctypes.c_int, _vp, ctypes.c_int64, ctypes.c_int,
                                          ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                          ctypes.c_float, _vp, _vp, _vpp, ctypes.c_int,
-                                         ctypes.c_int64, _vp]),
+                                         ctypes.c_int64, ctypes.c_int, _vp]),
     "ntp_gemm_set_pair": (ctypes.c_int, [ctypes.c_int]),
     "ntp_gemm_set_max_ctas": (ctypes.c_int, [ctypes.c_int]),
     "ntp_alloc": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, _vpp]),

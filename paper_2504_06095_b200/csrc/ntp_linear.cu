@@ -39,7 +39,7 @@ constexpr int kStages = 4;
 constexpr int kThreads = 192;   // 6 warps
 constexpr int kEpiWarp0 = 2;
 
-enum Epi { EPI_NONE = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_RED = 3 };
+enum Epi { EPI_NONE = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_RED = 3, EPI_PUSH = 4 };
 
 constexpr int kMaxPeers = 8;
 
@@ -157,6 +157,27 @@ struct Params {
   char *red_base[kMaxPeers];
   long long red_ld;        // elements
 };
+
+// 16-byte stores of 32 consecutive values (fp32 or bf16 destination, aligned)
+__device__ __forceinline__ void store_row32(void *dst, const float *f, int c_f32) {
+  if (c_f32) {
+    float4 *d = reinterpret_cast<float4 *>(dst);
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) d[j / 4] = make_float4(f[j], f[j + 1], f[j + 2], f[j + 3]);
+  } else {
+    uint4 *d = reinterpret_cast<uint4 *>(dst);
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        __nv_bfloat162 t = __floats2bfloat162_rn(f[j + 2 * e], f[j + 2 * e + 1]);
+        w[e] = *reinterpret_cast<uint32_t *>(&t);
+      }
+      d[j / 8] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
 
 // red.add of 32 consecutive values (fp32 or bf16 destination, 16-byte aligned)
 __device__ __forceinline__ void red_row32(void *dst, const float *f, int c_f32) {
@@ -433,18 +454,25 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         float f[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]) * p.alpha;
-        if (p.epi == EPI_RED) {
-          // fused sync: this replica's weighted contribution is added into its own
-          // copy and into the partner replica's copy of the same unit (peer HBM
-          // over NVLink); both copies start at zero, and two-term fp additions
-          // commute, so both replicas end with identical bits.
+        if (p.epi == EPI_RED || p.epi == EPI_PUSH) {
+          // fused sync: this replica's weighted contribution goes into its own copy
+          // and, over NVLink, into the partner replica's copy (EPI_RED: red.add
+          // into zeroed arenas) or the partner's staging arena (EPI_PUSH: plain
+          // stores; the partner adds staging into its arena after the done
+          // handshake).  Two-term fp sums commute: both replicas end bit-identical.
           if (row < p.M && col0 + 32 <= p.N) {
             const int ce = p.c_f32 ? 4 : 2;
-            red_row32(static_cast<char *>(p.C) + ((long long)row * p.ldc + col0) * ce, f, p.c_f32);
+            char *own = static_cast<char *>(p.C) + ((long long)row * p.ldc + col0) * ce;
             const int pb = p.red_buf[row];
-            if (pb >= 0)
-              red_row32(p.red_base[pb] + ((long long)p.red_row[row] * p.red_ld + col0) * ce, f,
-                        p.c_f32);
+            char *peer = pb >= 0 ? p.red_base[pb] + ((long long)p.red_row[row] * p.red_ld + col0) * ce
+                                 : nullptr;
+            if (p.epi == EPI_RED) {
+              red_row32(own, f, p.c_f32);
+              if (peer) red_row32(peer, f, p.c_f32);
+            } else {
+              store_row32(own, f, p.c_f32);
+              if (peer) store_row32(peer, f, p.c_f32);
+            }
           }
           continue;
         }
@@ -616,7 +644,8 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
   p.H = H;
   p.ldc = ldc;
   p.ldh = ldh;
-  p.c_tma = p.epi != EPI_RED && !((reinterpret_cast<uintptr_t>(C) & 15u) || ((ldc * ce) & 15));
+  p.c_tma = p.epi != EPI_RED && p.epi != EPI_PUSH &&
+            !((reinterpret_cast<uintptr_t>(C) & 15u) || ((ldc * ce) & 15));
   p.h_tma = p.epi == EPI_GELU && !((reinterpret_cast<uintptr_t>(H) & 15u) || ((ldh * 2) & 15));
   memset(&mc, 0, sizeof mc);
   memset(&mh, 0, sizeof mh);
@@ -694,8 +723,9 @@ extern "C" int ntp_gemm_bf16_red(const void *A, int64_t lda, int a_mn, const voi
                                  int64_t ldb, int b_mn, void *C, int64_t ldc, int c_f32,
                                  int64_t M, int64_t N, int64_t K, float alpha,
                                  const int32_t *red_buf, const int32_t *red_row,
-                                 void *const *red_base, int n_red, int64_t red_ld,
+                                 void *const *red_base, int n_red, int64_t red_ld, int mode,
                                  void *stream) {
+  if (mode != 0 && mode != 1) return fail(NTP_EINVAL, "fused mode must be 0 (red) or 1 (push)");
   if (M <= 0 || N <= 0 || K <= 0) return fail(NTP_EINVAL, "GEMM extents must be positive");
   if (N % 32) return fail(NTP_EINVAL, "fused sync GEMM needs N % 32 == 0");
   if (n_red < 0 || n_red > gemm::kMaxPeers) return fail(NTP_EINVAL, "at most 8 peer copies");
@@ -704,7 +734,8 @@ extern "C" int ntp_gemm_bf16_red(const void *A, int64_t lda, int a_mn, const voi
   if ((reinterpret_cast<uintptr_t>(C) & 15u) || ((ldc * ce) & 15) || ((red_ld * ce) & 15))
     return fail(NTP_EINVAL, "fused sync GEMM needs 16-byte aligned rows");
   gemm::Params p{(int)M, (int)N, (int)K, a_mn ? 1 : 0, b_mn ? 1 : 0, c_f32 ? 1 : 0,
-                 gemm::EPI_RED, nullptr, 0, alpha, 0, 0, nullptr, nullptr, 0, 0, 0, 0};
+                 mode ? gemm::EPI_PUSH : gemm::EPI_RED, nullptr, 0, alpha, 0, 0, nullptr,
+                 nullptr, 0, 0, 0, 0};
   p.red_buf = red_buf;
   p.red_row = red_row;
   for (int i = 0; i < gemm::kMaxPeers; ++i)

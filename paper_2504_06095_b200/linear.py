@@ -74,10 +74,13 @@ def mm(A: torch.Tensor, Bt: torch.Tensor, out: torch.Tensor, *, epilogue: str = 
 
 def mm_red(A: torch.Tensor, Bt: torch.Tensor, out: torch.Tensor, alpha: float,
            red_buf: torch.Tensor, red_row: torch.Tensor, red_bases, red_ld: int,
-           stream=None) -> None:
-    """Fused wgrad + sync: red.add(alpha * A @ Bt^T) into ``out`` (local copy) and
-    into row red_row[m] of red_bases[red_buf[m]] (the partner's copy); both must
-    start at zero.  red_buf/red_row: int32 device tensors [M]."""
+           stream=None, mode: str = "red") -> None:
+    """Fused wgrad + sync.  mode "red": red.add(alpha * A @ Bt^T) into ``out``
+    (local copy) and into row red_row[m] of red_bases[red_buf[m]] (the partner's
+    copy); both start at zero.  mode "push": plain stores into ``out`` and into
+    the partner's staging arena.  red_buf/red_row: int32 device tensors [M]."""
+    if mode not in ("red", "push"):
+        raise ValueError(f"unknown fused mode {mode!r}")
     M, K = A.shape
     N, K2 = Bt.shape
     if K != K2 or tuple(out.shape) != (M, N) or out.stride(1) != 1:
@@ -93,7 +96,8 @@ def mm_red(A: torch.Tensor, Bt: torch.Tensor, out: torch.Tensor, alpha: float,
         ctypes.c_void_p(out.data_ptr()), out.stride(0), int(out.dtype == torch.float32),
         M, N, K, float(alpha), ctypes.c_void_p(red_buf.data_ptr()),
         ctypes.c_void_p(red_row.data_ptr()), _lib.ptr_array(red_bases), len(red_bases),
-        int(red_ld), ctypes.c_void_p(stream.cuda_stream)), "ntp_gemm_bf16_red")
+        int(red_ld), 0 if mode == "red" else 1, ctypes.c_void_p(stream.cuda_stream)),
+        "ntp_gemm_bf16_red")
 
 
 def partner_row_map(cols, partner_cols, device):
@@ -155,11 +159,12 @@ class MlpShard:
 
     def backward_synced(self, X: torch.Tensor, G: torch.Tensor, grads: torch.Tensor, alpha: float,
                         red_buf: torch.Tensor, red_row: torch.Tensor, partner_arenas,
-                        stream=None) -> None:
+                        stream=None, mode: str = "red") -> None:
         """backward() with the NTP sync fused into the weight-gradient epilogues:
-        alpha * dB, alpha * dA^T are red.add-ed into this rank's unit-major arena
-        and into the partner replica's arenas (zeroed beforehand).  After both
-        replicas' fused backward the arenas hold w_h*g_h + w_r*g_r."""
+        alpha * dB, alpha * dA^T go into this rank's unit-major arena and into the
+        partner replica's arenas -- red.add into zeroed arenas (mode "red"), or
+        stores into the partner's staging arenas (mode "push", finished by
+        ``finish_push``).  Afterwards both replicas hold w_h*g_h + w_r*g_r."""
         T = X.shape[0]
         H, Y = self.H[:, :self.n], self.Y[:, :self.n]
         Dfull = torch.empty((T, _pad8(self.n)), dtype=torch.bfloat16, device=X.device)
@@ -169,8 +174,25 @@ class MlpShard:
         h = self.h
         bases_b = [int(t.data_ptr()) + h * eb for t in partner_arenas]
         bases_a = [int(t.data_ptr()) for t in partner_arenas]
-        mm_red(Y.T, G.T, grads[:, 1, :], alpha, red_buf, red_row, bases_b, 2 * h, stream)
-        mm_red(D.T, X.T, grads[:, 0, :], alpha, red_buf, red_row, bases_a, 2 * h, stream)
+        mm_red(Y.T, G.T, grads[:, 1, :], alpha, red_buf, red_row, bases_b, 2 * h, stream, mode)
+        mm_red(D.T, X.T, grads[:, 0, :], alpha, red_buf, red_row, bases_a, 2 * h, stream, mode)
+
+
+_FINISH_PLANS: dict = {}
+
+
+def finish_push(arena: torch.Tensor, staging: torch.Tensor, stream=None) -> None:
+    """arena += staging (fp32 accumulation, arena operand first on both replicas'
+    sides so the two copies add the same two terms) -- the local tail of the
+    "push" fused sync, after the partners' done signal."""
+    from .plans import OPS, Plan, dtype_code
+    n, dt, dev = arena.numel(), arena.dtype, arena.device.index
+    key = (n, dt, dev)
+    plan = _FINISH_PLANS.get(key)
+    if plan is None:
+        plan = Plan(dtype_code(dt)).add_units(n, [0], [0], [1], [0]).finalize().upload(dev)
+        _FINISH_PLANS[key] = plan
+    plan.grad_sync_into([arena.data_ptr(), staging.data_ptr()], OPS["sum"], 1.0, 1.0, 1, stream)
 
 
 def mlp_forward_tp(X: torch.Tensor, shards) -> torch.Tensor:

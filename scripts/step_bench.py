@@ -53,6 +53,7 @@ def run_config(args, n1, n2, local):
     tok_r = args.tokens * n2 // n1
     w_h, w_r = tok_h / (tok_h + tok_r), tok_r / (tok_h + tok_r)
     groups = [NtpSyncGroup(lay, plc, torch.bfloat16, local).upload() for _ in range(L)]
+    staging = [NtpSyncGroup(lay, plc, torch.bfloat16, local).upload() for _ in range(L)]
     g = torch.Generator(device="cuda").manual_seed(rank)
     rng = np.random.default_rng(rank)
     shards = []   # per layer: [(shard, X, G, grads_view)]
@@ -110,8 +111,10 @@ def run_config(args, n1, n2, local):
             partner_cols = rc if healthy else hc
             partner_slots = [n1 + j for j in range(n2)] if healthy else list(range(n1))
             ptrs = groups[li].open_slots(partner_slots)
+            sptrs = staging[li].open_slots(partner_slots)
             rb, rr = partner_row_map(cols, partner_cols, "cuda")
-            per.append((sh, X, G, grads, w_h if healthy else w_r, rb, rr, ptrs))
+            per.append((sh, X, G, grads, w_h if healthy else w_r, rb, rr, ptrs, sptrs,
+                        staging[li].arena(s)))
         fused.append(per)
 
     class _P:  # raw pointer holder with the .data_ptr() mm_red expects
@@ -121,20 +124,27 @@ def run_config(args, n1, n2, local):
         def data_ptr(self):
             return self.p
 
-    def fused_backward():
+    from paper_2504_06095_b200.linear import finish_push
+
+    def fused_backward(mode="red"):
         for li in range(L):
             gr = groups[li]
             gr.epoch += 1
-            for s in gr.hosted:
-                gr.arena(s).zero_()
+            if mode == "red":
+                for s in gr.hosted:
+                    gr.arena(s).zero_()
             gr.signal("post_ready", gr.epoch, main)
             gr.signal("wait_ready", gr.epoch, main)
         for li in reversed(range(L)):
-            for sh, X, G, grads, alpha, rb, rr, ptrs in fused[li]:
-                sh.backward_synced(X, G, grads, alpha, rb, rr, [_P(p) for p in ptrs], main)
+            for sh, X, G, grads, alpha, rb, rr, ptrs, sptrs, st in fused[li]:
+                tgt = ptrs if mode == "red" else sptrs
+                sh.backward_synced(X, G, grads, alpha, rb, rr, [_P(p) for p in tgt], main, mode)
             groups[li].signal("post_done", groups[li].epoch, main)
         for li in range(L):
             groups[li].signal("wait_done", groups[li].epoch, main)
+            if mode == "push":
+                for sh, X, G, grads, alpha, rb, rr, ptrs, sptrs, st in fused[li]:
+                    finish_push(grads, st, main)
 
     def timed(fn, iters):
         for _ in range(2):
@@ -158,6 +168,7 @@ def run_config(args, n1, n2, local):
     res["sync_ms"] = round(timed(sync_only, args.iters), 3)
     res["serial_ms"] = round(timed(lambda: backward(False), args.iters), 3)
     res["fused_wgrad_sync_ms"] = round(timed(fused_backward, args.iters), 3)
+    res["fused_push_wgrad_sync_ms"] = round(timed(lambda: fused_backward("push"), args.iters), 3)
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     for cap in args.caps:
         # TMA-bulk sync (131 KB smem/CTA): it cannot share an SM with a GEMM CTA,
@@ -175,7 +186,7 @@ def run_config(args, n1, n2, local):
         res[f"overlap_ms_ldg_cap{cap}"] = round(timed(lambda: backward(True), args.iters), 3)
     Lb.ntp_set_option(0, 0)
     Lb.ntp_set_option(1, 0)
-    for gr in groups:
+    for gr in groups + staging:
         assert gr.status() == 0, "signal timeout"
         gr.close()
     return res

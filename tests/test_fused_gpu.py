@@ -71,3 +71,48 @@ def test_fused_backward_sync_matches_unfused(mods, gdtype, tol):
     da2, db2 = O.mlp_backward(Xr, A, B, Gr)
     assert O.rel_err(dh[0], w_h * da1 + w_r * da2) < 2e-2
     assert O.rel_err(dh[1], w_h * db1 + w_r * db2) < 2e-2
+
+
+@pytest.mark.parametrize("gdtype,tol", [(torch.float32, 1e-5), (torch.bfloat16, 1e-2)])
+def test_fused_push_mode(mods, gdtype, tol):
+    """mode "push": plain stores into the partner's staging arena, then each
+    replica adds its staging locally -- same result, replicas bit-identical."""
+    Lin, T = mods
+    from paper_2504_06095_b200.shardmap import build_shard_map
+    h, k, tok_h, tok_r = 128, 600, 256, 192
+    A, B = O.random_layer(h, k, seed=21)
+    A, B = A / np.sqrt(h), B / np.sqrt(k)
+    bf = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(torch.bfloat16)  # noqa: E731
+    r64 = lambda x: bf(x).double().numpy()  # noqa: E731
+    A, B = r64(A), r64(B)
+    rng = np.random.default_rng(22)
+    Xh, Gh = (r64(rng.standard_normal((tok_h, h))) for _ in range(2))
+    Xr, Gr = (r64(rng.standard_normal((tok_r, h))) for _ in range(2))
+    smap = build_shard_map(k, 4, 3)
+    hc, rc = T.assignment_from_comp(smap), T.assignment_from_sync(smap)
+    w_h, w_r = tok_h / (tok_h + tok_r), tok_r / (tok_h + tok_r)
+    layer = T.MlpLayer(A, B)
+    sh_h = [Lin.MlpShard(A, B, c) for c in hc]
+    sh_r = [Lin.MlpShard(A, B, c) for c in rc]
+    for sh in sh_h:
+        sh.forward(bf(Xh).cuda(), torch.empty((tok_h, h), device="cuda"))
+    for sh in sh_r:
+        sh.forward(bf(Xr).cuda(), torch.empty((tok_r, h), device="cuda"))
+    fh, fr = T.MlpReplica(layer, hc, dtype=gdtype), T.MlpReplica(layer, rc, dtype=gdtype)
+    sth, stf = T.MlpReplica(layer, hc, dtype=gdtype), T.MlpReplica(layer, rc, dtype=gdtype)
+    for sh, cols, g in zip(sh_h, hc, fh.grads):
+        rb, rr = Lin.partner_row_map(cols, rc, "cuda")
+        sh.backward_synced(bf(Xh).cuda(), bf(Gh).cuda(), g, w_h, rb, rr, stf.grads, mode="push")
+    for sh, cols, g in zip(sh_r, rc, fr.grads):
+        rb, rr = Lin.partner_row_map(cols, hc, "cuda")
+        sh.backward_synced(bf(Xr).cuda(), bf(Gr).cuda(), g, w_r, rb, rr, sth.grads, mode="push")
+    for g, s in zip(fh.grads + fr.grads, sth.grads + stf.grads):
+        Lin.finish_push(g, s)
+    fh._has_grads = fr._has_grads = True
+    torch.cuda.synchronize()
+    dh, dr = fh.dense_grads(), fr.dense_grads()
+    assert np.array_equal(dh[0], dr[0]) and np.array_equal(dh[1], dr[1])
+    da1, db1 = O.mlp_backward(Xh, A, B, Gh)
+    da2, db2 = O.mlp_backward(Xr, A, B, Gr)
+    assert O.rel_err(dh[0], w_h * da1 + w_r * da2) < 2e-2
+    assert O.rel_err(dh[1], w_h * db1 + w_r * db2) < 2e-2
