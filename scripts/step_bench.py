@@ -99,6 +99,30 @@ def run_config(args, n1, n2, local):
         for li in reversed(range(L)):
             groups[li].step(w_h, w_r, main)
 
+    def timeline():
+        """One overlapped backward with events: per layer, when its GEMMs and its
+        sync finished (ms from the start), on this rank."""
+        t0 = torch.cuda.Event(enable_timing=True)
+        g_end, s_end = [], []
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0.record(main)
+        for li in reversed(range(L)):
+            for sh, X, G, grads in shards[li]:
+                sh.backward(X, G, grads)
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(main)
+            g_end.append(e)
+            side.wait_event(e)
+            groups[li].step(w_h, w_r, side)
+            e2 = torch.cuda.Event(enable_timing=True)
+            e2.record(side)
+            s_end.append(e2)
+        main.wait_stream(side)
+        torch.cuda.synchronize()
+        return {"gemm_done_ms": [round(t0.elapsed_time(e), 3) for e in g_end],
+                "sync_done_ms": [round(t0.elapsed_time(e), 3) for e in s_end]}
+
     # fused wgrad + sync: every GPU's wgrad epilogue red.adds its weighted
     # gradient into its own arena and the partner replica's (zeroed first)
     from paper_2504_06095_b200.linear import partner_row_map
@@ -184,6 +208,14 @@ def run_config(args, n1, n2, local):
         Lb.ntp_set_option(0, 1)
         Lb.ntp_set_option(1, cap)
         res[f"overlap_ms_ldg_cap{cap}"] = round(timed(lambda: backward(True), args.iters), 3)
+    Lb.ntp_set_option(0, 1)
+    Lb.ntp_set_option(1, 74)
+    for _ in range(2):
+        timeline()
+    tl = timeline()
+    allt = [None] * dist.get_world_size()
+    dist.all_gather_object(allt, tl)
+    res["timeline_ldg_cap74_per_rank"] = allt
     Lb.ntp_set_option(0, 0)
     Lb.ntp_set_option(1, 0)
     for gr in groups + staging:
