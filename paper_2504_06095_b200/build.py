@@ -33,19 +33,28 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile (if stale or forced).  Concurrent callers -- e.g. the ranks of a
+    torchrun job -- serialize on a file lock and each writes its own temporary,
+    so the in-tree .so is replaced atomically exactly once."""
+    import fcntl
     if not force and not _stale():
         return LIB
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared",
-           "-Xcompiler", "-fPIC,-O3,-Wall", "-cudart", "static",
-           "-I", os.path.join(ROOT, "include"), "-Xptxas", "-v" if verbose else "-O3",
-           "-o", LIB + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libntp_b200.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
-    os.replace(LIB + ".tmp", LIB)
+    with open(LIB + ".lock", "w") as lock:
+        fcntl.flock(lock, fcntl.LOCK_EX)
+        if not force and not _stale():  # another process built it meanwhile
+            return LIB
+        tmp = f"{LIB}.{os.getpid()}.tmp"
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared",
+               "-Xcompiler", "-fPIC,-O3,-Wall", "-cudart", "static",
+               "-I", os.path.join(ROOT, "include"), "-Xptxas", "-v" if verbose else "-O3",
+               "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc failed building libntp_b200.so")
+        if verbose:
+            sys.stderr.write(r.stderr)
+        os.replace(tmp, LIB)
     return LIB
 
 
