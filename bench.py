@@ -233,11 +233,20 @@ def run_e2e_single(args, lay, plan, dtype, eb):
     import torch
     from paper_2504_06095_b200.hostsync import HostSync
     from paper_2504_06095_b200.workloads import layer_pieces
+    lpp = int(os.environ.get("NTP_E2E_LAYERS_PER_PIECE", "1"))
     hs = HostSync(plan, [e for e in lay.h_elems + lay.r_elems], dtype, device=0,
-                  piece_plans=layer_pieces(lay, dtype, 0, layers_per_piece=2))
+                  piece_plans=layer_pieces(lay, dtype, 0, layers_per_piece=lpp))
     gen = torch.Generator().manual_seed(1)
     host = [torch.randn(e, generator=gen, dtype=torch.float32).to(dtype).pin_memory()
             for e in lay.h_elems + lay.r_elems]
+    # host-link context: one direction alone, the same bytes as a step's H2D
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for d, h in zip(hs.arenas, host):
+        d.copy_(h, non_blocking=True)
+    s1.record()
+    torch.cuda.synchronize()
+    h2d_gbs = sum(h.numel() for h in host) * eb / (s0.elapsed_time(s1) * 1e-3) / 1e9
     steps = max(2, min(args.e2e_steps, args.steps))
     for _ in range(2):
         hs.run(host, W_H, W_R)
@@ -255,7 +264,10 @@ def run_e2e_single(args, lay, plan, dtype, eb):
             "ms_per_step": round(ms, 3), "steps": steps,
             "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
             "wall_ms_per_step": round((time.perf_counter() - t0) * 1e3 / steps, 3),
-            "gpu_launches_per_step": hs.launches_per_run}
+            "gpu_launches_per_step": hs.launches_per_run,
+            "pipeline_pieces": len(hs.pieces or []),
+            "host_link_h2d_only_gbs": round(h2d_gbs, 1),
+            "host_link_bound_ms": round(nbytes / (h2d_gbs * 1e9) * 1e3, 2)}
 
 
 def _ncu_traffic():
