@@ -363,3 +363,68 @@ def multi_grad_sync(replicas, op: str = "sum", weights=None) -> None:
     plan = MultiPlan(dtype_code(first.dtype), len(replicas)).add_units(unit, bufs, offs)
     plan.finalize().upload(dev)
     plan.sync(tensor_ptrs([g for rep in replicas for g in rep.grads]), code, weights)
+
+
+# ---------------------------------------------------------------------------
+# attention heads as sync units.  The reference shards
+# attention by whole heads (AttentionReplica, tpnumerics.py:158-167) but has no
+# attention gradients; here a head's four blocks (wq, wk, wv: [hidden x hd],
+# wo: [hd x hidden]) form one contiguous unit of 4*hidden*hd elements
+# (perfmodel.py:270-272) and heads sync exactly like MLP columns.
+
+
+class AttentionReplica:
+    """Per-rank head ownership (tpnumerics.py:158-167) plus device-resident
+    head-unit gradients ``grads[r]`` = [n_heads_r, 4, hidden, head_dim] (wo's
+    block stored transposed so every head is one contiguous unit)."""
+
+    def __init__(self, layer, head_assignment, *, dtype: torch.dtype = torch.bfloat16,
+                 device=None):
+        heads = np.concatenate([np.asarray(a, dtype=np.int64) for a in head_assignment])
+        if len(heads) != layer.heads or len(np.unique(heads)) != layer.heads:
+            raise ValueError("assignment does not partition the heads exactly once")
+        self.layer = layer
+        self.n = len(head_assignment)
+        self.heads = [np.asarray(a, dtype=np.int64) for a in head_assignment]
+        self.dtype = dtype
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None \
+            else torch.device(device)
+        self.unit = 4 * layer.hidden * layer.head_dim
+        self.grads = [torch.zeros((len(h), 4, layer.hidden, layer.head_dim), dtype=dtype,
+                                  device=self.device) for h in self.heads]
+        self._has_grads = False
+
+    def set_units(self, units) -> "AttentionReplica":
+        for g, u in zip(self.grads, units):
+            t = u if torch.is_tensor(u) else torch.from_numpy(np.ascontiguousarray(u))
+            g.view(-1).copy_(t.reshape(-1).to(self.device, self.dtype))
+        self._has_grads = True
+        return self
+
+    def units(self) -> list[np.ndarray]:
+        return [g.reshape(g.shape[0], -1).to(torch.float64).cpu().numpy() for g in self.grads]
+
+
+def nonuniform_head_sync(healthy: AttentionReplica, reduced: AttentionReplica, smap: ShardMap,
+                         op: str = "sum", weights=None) -> None:
+    """nonuniform_grad_sync (tpnumerics.py:289-356) over attention heads: the
+    shard map is built over k = heads (shardmap.py:141-182, attention_head_partition
+    gives the same balanced counts) and every head is one unit."""
+    if healthy.n != smap.n1 or reduced.n != smap.n2:
+        raise ValueError(
+            f"replica degrees ({healthy.n}, {reduced.n}) do not match map ({smap.n1}, {smap.n2})")
+    if healthy.layer.heads != smap.k:
+        raise ValueError(f"map is over k={smap.k} heads, layer has {healthy.layer.heads}")
+    for r in range(smap.n1):
+        if not np.array_equal(np.sort(healthy.heads[r]), smap.comp_columns(r)):
+            raise ValueError("healthy replica is not sharded by the map's comp layout")
+    for r in range(smap.n2):
+        if not np.array_equal(np.sort(reduced.heads[r]), smap.sync_columns(r)):
+            raise ValueError("reduced replica is not sharded by the map's sync layout")
+    if not (healthy._has_grads and reduced._has_grads):
+        raise ValueError("both replicas must hold gradients")
+    code, w_h, w_r = _op_and_weights(op, weights)
+    dev = healthy.device.index if healthy.device.index is not None else torch.cuda.current_device()
+    plan = build_pair_plan(healthy.heads, reduced.heads, smap.k, healthy.unit,
+                           dtype_code(healthy.dtype)).finalize().upload(dev)
+    plan.grad_sync(tensor_ptrs(healthy.grads + reduced.grads), code, w_h, w_r)
