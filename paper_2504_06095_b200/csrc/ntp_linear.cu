@@ -27,6 +27,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "ntp_internal.h"
 
@@ -35,9 +37,7 @@ namespace gemm {
 
 constexpr int BM = 128;
 constexpr int BK = 64;          // 64 bf16 = 128 B: one swizzle-128B row
-constexpr int kStages = 4;
-constexpr int kThreads = 192;   // 6 warps
-constexpr int kEpiWarp0 = 2;
+constexpr int kThreads = 192;   // 6 warps: TMA, MMA, 4 x epilogue
 
 enum Epi { EPI_NONE = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_RED = 3, EPI_PUSH = 4 };
 
@@ -156,7 +156,33 @@ struct Params {
   const int *red_row;
   char *red_base[kMaxPeers];
   long long red_ld;        // elements
+  // split-K tail: tiles [0, full_items) run whole; each of the remaining tiles is
+  // cut into `split` K ranges run by different CTA pairs, whose fp32 partials
+  // meet in `ws`; the last arriving piece of each warp slice sums and stores
+  int full_items, split;
+  int *tile_cnt;
+  float *ws;
+  // debug only (ntp_gemm_debug_trace): per (CTA, local item) 8 u64:
+  // {item, t_full, t_done, t_kernel_start, t_prod_first, t_prod_last, t_mma_first, t_mma_last}
+  unsigned long long *trace;
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+constexpr int kTraceItems = 16;
+
+struct Work {
+  int t, kb_lo, kb_hi, tail, piece;
+};
+
+__device__ __forceinline__ Work decode_work(int item, const Params &p, int nk) {
+  if (item < p.full_items) return Work{item, 0, nk, -1, 0};
+  const int j = item - p.full_items, tail = j / p.split, piece = j % p.split;
+  return Work{p.full_items + tail, nk * piece / p.split, nk * (piece + 1) / p.split, tail, piece};
+}
 
 // 16-byte stores of 32 consecutive values (fp32 or bf16 destination, aligned)
 __device__ __forceinline__ void store_row32(void *dst, const float *f, int c_f32) {
@@ -230,7 +256,7 @@ template <int BN, int kPair, int kStg>
 struct Smem {
   alignas(1024) __nv_bfloat16 a[kStg][BM * BK];
   alignas(1024) __nv_bfloat16 b[kStg][(BN / kPair) * BK];
-  alignas(128) unsigned char out[4][kStageBytes];
+  alignas(128) unsigned char out[4][2][kStageBytes];  // double-buffered per epilogue warp
   uint64_t full[kStg];
   uint64_t empty[kStg];
   uint64_t tmem_full[2];
@@ -314,6 +340,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   const int lane = threadIdx.x & 31;
   const int nk = (p.K + BK - 1) / BK;
   const int num_tiles = p.num_m * p.num_n;
+  const int num_items = p.full_items + (num_tiles - p.full_items) * p.split;
   const uint32_t rank = kPair == 2 ? cluster_rank() : 0u;
   const bool leader = rank == 0;
   const int unit_id = blockIdx.x / kPair, num_units = gridDim.x / kPair;
@@ -346,18 +373,25 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   if constexpr (kPair == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
+  if (p.trace && threadIdx.x == 0) p.trace[(size_t)blockIdx.x * kTraceItems * 8 + 3] = gtime();
 
   if (warp == 0) {
     if (lane == 0) {
       // ---- TMA producer (both CTAs of a pair) ----
       const uint32_t cta_bytes = (BM + BNC) * BK * 2;
-      int it = 0;
-      for (int t = unit_id; t < num_tiles; t += num_units) {
+      int it = 0, plocal = 0;
+      for (int item = unit_id; item < num_items; item += num_units, ++plocal) {
+        const Work w = decode_work(item, p, nk);
+        const int t = w.t;
         const int m0 = (t % p.num_m) * TM + (int)rank * BM;
         const int n0 = (t / p.num_m) * BN + (int)rank * BNC;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        unsigned long long *trp =
+            p.trace && plocal < kTraceItems ? p.trace + ((size_t)blockIdx.x * kTraceItems + plocal) * 8 : nullptr;
+        for (int kb = w.kb_lo; kb < w.kb_hi; ++kb, ++it) {
           const int s = it % kStg;
           mbar_wait(&sm.empty[s], ((it / kStg) & 1) ^ 1);
+          if (trp && kb == w.kb_lo) trp[4] = gtime();
+          if (trp && kb == w.kb_hi - 1) trp[5] = gtime();
           if (leader) mbar_expect_tx(&sm.full[s], cta_bytes * kPair);
           const int k0 = kb * BK;
           auto load = [&](void *dst, const CUtensorMap *m, int c0, int c1) {
@@ -389,22 +423,28 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       const uint32_t a_lbo = p.a_mn ? BK * 128 : 16, b_lbo = p.b_mn ? BK * 128 : 16;
       const uint32_t k_step_a = p.a_mn ? 2048u : 32u, k_step_b = p.b_mn ? 2048u : 32u;
       int it = 0, local = 0;
-      for (int t = unit_id; t < num_tiles; t += num_units, ++local) {
+      for (int item = unit_id; item < num_items; item += num_units, ++local) {
+        const Work w = decode_work(item, p, nk);
         const int acc = local & 1;
         mbar_wait(&sm.tmem_empty[acc], ((local >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(acc * BN);
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        unsigned long long *trp =
+            p.trace && local < kTraceItems ? p.trace + ((size_t)blockIdx.x * kTraceItems + local) * 8 : nullptr;
+        for (int kb = w.kb_lo; kb < w.kb_hi; ++kb, ++it) {
           const int s = it % kStg;
           mbar_wait(&sm.full[s], (it / kStg) & 1);
+          if (trp && kb == w.kb_lo) trp[6] = gtime();
+          if (trp && kb == w.kb_hi - 1) trp[7] = gtime();
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sm.a[s]), b_addr = smem_u32(sm.b[s]);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ad = smem_desc(a_addr + kk * k_step_a, a_lbo, 1024);
             const uint64_t bd = smem_desc(b_addr + kk * k_step_b, b_lbo, 1024);
-            if constexpr (kPair == 2) tc_mma2(d, ad, bd, idesc, (kb | kk) ? 1u : 0u);
-            else tc_mma(d, ad, bd, idesc, (kb | kk) ? 1u : 0u);
+            const uint32_t accum = (kb > w.kb_lo || kk) ? 1u : 0u;
+            if constexpr (kPair == 2) tc_mma2(d, ad, bd, idesc, accum);
+            else tc_mma(d, ad, bd, idesc, accum);
           }
           // frees the stage (in both CTAs) once these MMAs have read it
           if constexpr (kPair == 2) tc_commit2(&sm.empty[s], 0x3); else tc_commit(&sm.empty[s]);
@@ -415,45 +455,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   } else {
     // ---- epilogue: TMEM -> registers -> fused op -> smem -> TMA store ----
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    unsigned char *stage = sm.out[q];
+    int sbuf = 0;
     int local = 0;
-    for (int t = unit_id; t < num_tiles; t += num_units, ++local) {
-      const int acc = local & 1;
-      const int m0 = (t % p.num_m) * TM + (int)rank * BM, n0 = (t / p.num_m) * BN;
-      const int row0 = m0 + q * 32;
+    // one 32-column chunk of this warp's 32-row slice: raw fp32 sums -> fused
+    // epilogue -> global (TMA store, warp copy, or fused-sync stores)
+    auto emit = [&](const int n0, const int row0, const int c, float *f) {
       const int row = row0 + lane;
-      mbar_wait(&sm.tmem_full[acc], (local >> 1) & 1);
-      tc_fence_after();
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t v[32];
-        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, "
-            "%10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, "
-            "%27, %28, %29, %30, %31}, [%32];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-              "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
-              "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
-              "=r"(v[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (c + 32 >= BN) {
-          // all of this accumulator has been read: hand it back to the MMA warp
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) {
-            if constexpr (kPair == 2) mbar_arrive_cluster(&sm.tmem_empty[acc], 0);
-            else mbar_arrive(&sm.tmem_empty[acc]);
-          }
-        }
         const int col0 = n0 + c;
-        if (col0 >= p.N || row0 >= p.M) continue;  // warp-uniform: nothing of this box is stored
-        float f[32];
+        if (col0 >= p.N || row0 >= p.M) return;  // warp-uniform: nothing of this box is stored
 #pragma unroll
-        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]) * p.alpha;
+        for (int j = 0; j < 32; ++j) f[j] *= p.alpha;
         if (p.epi == EPI_RED || p.epi == EPI_PUSH) {
           // fused sync: this replica's weighted contribution goes into its own copy
           // and, over NVLink, into the partner replica's copy (EPI_RED: red.add
@@ -474,10 +485,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
               if (peer) store_row32(peer, f, p.c_f32);
             }
           }
-          continue;
+          return;
         }
-        // the previous TMA store of this warp must have finished reading `stage`
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        // staging alternates between two boxes: the store issued two boxes ago
+        // (the last-but-one bulk group) must have finished reading this one
+        unsigned char *stage = sm.out[q][sbuf];
+        sbuf ^= 1;
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         __syncwarp();
         if (p.epi == EPI_GELU) {
           // H = bf16(acc) (kept for the backward), Y = GeLU(H)
@@ -548,7 +562,122 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         if (p.epi == EPI_GELU && !p.h_tma)
           box_store(stage + 2048, p.H, p.ldh, 2, row0, col0, p.M, p.N, lane);
         __syncwarp();
+    };
+    for (int item = unit_id; item < num_items; item += num_units, ++local) {
+      const Work w = decode_work(item, p, nk);
+      const int t = w.t;
+      const int acc = local & 1;
+      const int m0 = (t % p.num_m) * TM + (int)rank * BM, n0 = (t / p.num_m) * BN;
+      const int row0 = m0 + q * 32;
+      // split-K piece: this warp's 32 x BN partial lives in ws, float4 column
+      // groups outermost so each warp access is 512 contiguous bytes
+      float4 *slice = w.tail >= 0
+          ? reinterpret_cast<float4 *>(
+                p.ws + ((((size_t)w.tail * p.split + w.piece) * kPair + rank) * 4 + q) * 32 * BN)
+          : nullptr;
+      mbar_wait(&sm.tmem_full[acc], (local >> 1) & 1);
+      const bool tr = p.trace && q == 0 && lane == 0 && local < kTraceItems;
+      unsigned long long *trp = tr ? p.trace + ((size_t)blockIdx.x * kTraceItems + local) * 8 : nullptr;
+      if (tr) { trp[0] = (unsigned long long)item; trp[1] = gtime(); }
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, "
+            "%10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, "
+            "%27, %28, %29, %30, %31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+              "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+              "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+              "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c + 32 >= BN) {
+          // all of this accumulator has been read: hand it back to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (kPair == 2) mbar_arrive_cluster(&sm.tmem_empty[acc], 0);
+            else mbar_arrive(&sm.tmem_empty[acc]);
+          }
+        }
+        if (slice) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            __stcg(slice + (c / 4 + j / 4) * 32 + lane,
+                   make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                               __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3])));
+        } else {
+          float f[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+          emit(n0, row0, c, f);
+        }
       }
+      if (slice) {
+        // Distributed fixup: the `split` pieces of this warp slice meet at a
+        // counter (all of them run in the final wave of this persistent grid),
+        // then piece i sums every partial, in piece order (deterministic), for
+        // the 32-column chunks i, i+split, ... and runs their epilogue.
+        __threadfence();
+        __syncwarp();
+        int *cnt = p.tile_cnt + (((size_t)w.tail * kPair + rank) * 4 + q) * 2;
+        if (lane == 0) {
+          atomicAdd(cnt, 1);
+          const unsigned long long t0 = gtime();
+          for (;;) {
+            int n;
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(n) : "l"(cnt) : "memory");
+            if (n >= p.split) break;
+            if (gtime() - t0 > 4000000000ull) asm volatile("trap;");
+          }
+        }
+        __syncwarp();
+        __threadfence();
+        const size_t piece_stride = (size_t)kPair * BM * BN / 4;  // float4s
+        const float4 *base = slice - (size_t)w.piece * piece_stride;
+#pragma unroll 1
+        for (int c = w.piece * 32; c < BN; c += 32 * p.split) {
+          float f[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) f[j] = 0.0f;
+          int pc = 0;
+          for (; pc + 1 < p.split; pc += 2) {  // two partials' loads in flight
+            float4 x[8], y[8];
+            const float4 *s0 = base + pc * piece_stride + (c / 4) * 32 + lane;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              x[j] = __ldcg(s0 + j * 32);
+              y[j] = __ldcg(s0 + piece_stride + j * 32);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              f[4 * j] += x[j].x; f[4 * j + 1] += x[j].y; f[4 * j + 2] += x[j].z; f[4 * j + 3] += x[j].w;
+              f[4 * j] += y[j].x; f[4 * j + 1] += y[j].y; f[4 * j + 2] += y[j].z; f[4 * j + 3] += y[j].w;
+            }
+          }
+          if (pc < p.split) {
+            const float4 *s0 = base + pc * piece_stride + (c / 4) * 32 + lane;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 x = __ldcg(s0 + j * 32);
+              f[4 * j] += x.x; f[4 * j + 1] += x.y; f[4 * j + 2] += x.z; f[4 * j + 3] += x.w;
+            }
+          }
+          emit(n0, row0, c, f);
+        }
+        // the last piece to leave resets both counters for the next launch
+        __syncwarp();
+        if (lane == 0 && atomicAdd(cnt + 1, 1) == p.split - 1) {
+          cnt[0] = 0;
+          cnt[1] = 0;
+        }
+      }
+      if (tr) trp[2] = gtime();
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
@@ -623,6 +752,50 @@ static int sm_count_dev() {
 
 static std::atomic<int> g_pair{1};
 static std::atomic<int> g_max_ctas{0};
+static std::atomic<int> g_split_k{1};
+static unsigned long long *g_trace = nullptr;
+
+// Split-K partials and per-slice arrival counters, one set per (device, stream)
+// so GEMMs on different streams never share them.  Grow-only; counters are
+// zeroed on allocation and reset by the last arriving piece.
+struct Workspace {
+  float *ws = nullptr;
+  int *cnt = nullptr;
+  size_t ws_bytes = 0, cnt_bytes = 0;
+  int ensure(size_t need_ws, size_t need_cnt, cudaStream_t s) {
+    if (need_ws > ws_bytes) {
+      if (ws) cudaFree(ws);
+      if (cudaMalloc(&ws, need_ws) != cudaSuccess) {
+        ws = nullptr;
+        ws_bytes = 0;
+        return fail(NTP_ECUDA, "split-K workspace allocation failed");
+      }
+      ws_bytes = need_ws;
+    }
+    if (need_cnt > cnt_bytes) {
+      if (cnt) cudaFree(cnt);
+      if (cudaMalloc(&cnt, need_cnt) != cudaSuccess || cudaMemsetAsync(cnt, 0, need_cnt, s) != cudaSuccess) {
+        cnt = nullptr;
+        cnt_bytes = 0;
+        return fail(NTP_ECUDA, "split-K counter allocation failed");
+      }
+      cnt_bytes = need_cnt;
+    }
+    return NTP_OK;
+  }
+};
+
+static Workspace &workspace_for(cudaStream_t s) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, cudaStream_t>, Workspace *>> table;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  for (auto &e : table)
+    if (e.first.first == dev && e.first.second == s) return *e.second;
+  table.push_back({{dev, s}, new Workspace()});
+  return *table.back().second;
+}
 
 template <int BN, int kPair, int kStg>
 static int launch(const void *A, long long lda, int a_mn, const void *B, long long ldb, int b_mn,
@@ -669,7 +842,38 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
   const int cap = g_max_ctas.load();
   if (cap > 0 && cap < sms) sms = cap;  // leave SMs to a concurrent sync kernel
   const int units = sms / kPair > 0 ? sms / kPair : 1;
-  const int grid = (tiles < units ? tiles : units) * kPair;
+  // split-K for the last, partial wave: its R tiles are cut into S K-ranges so
+  // the wave is filled instead of leaving most SMs idle for a whole tile time
+  p.full_items = tiles;
+  p.split = 1;
+  p.tile_cnt = nullptr;
+  p.ws = nullptr;
+  p.trace = g_trace;
+  const int rem = tiles % units, nkb = (p.K + BK - 1) / BK;
+  if (g_split_k.load() && rem > 0) {
+    const int cap_s = g_split_k.load() >= 2 ? g_split_k.load() : 8;
+    int S = units / rem;
+    if (S > cap_s) S = cap_s;          // bound the fixup's partial reads
+    if (S > nkb / 4) S = nkb / 4;      // >= 4 k-blocks per piece
+    if (S > BN / 32) S = BN / 32;      // every piece fixes up >= 1 column chunk
+    Workspace &w = workspace_for(s);
+    const size_t need_ws = (size_t)rem * S * kPair * BM * BN * sizeof(float);
+    const size_t need_cnt = (size_t)rem * kPair * 4 * 2 * sizeof(int);
+    cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap_st);
+    // never allocate inside a graph capture: run whole tiles instead
+    const bool fits = need_ws <= w.ws_bytes && need_cnt <= w.cnt_bytes;
+    if (S >= 2 && (fits || cap_st == cudaStreamCaptureStatusNone)) {
+      int st2 = w.ensure(need_ws, need_cnt, s);
+      if (st2) return st2;
+      p.full_items = tiles - rem;
+      p.split = S;
+      p.ws = w.ws;
+      p.tile_cnt = w.cnt;
+    }
+  }
+  const int items = p.full_items + (tiles - p.full_items) * p.split;
+  const int grid = (items < units ? items : units) * kPair;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -783,6 +987,21 @@ int dispatch(const void *A, long long lda, int a_mn, const void *B, long long ld
 
 // 1 (default): 256-row CTA-pair tiles (tcgen05 cta_group::2) for N > 128; 0: 1-SM tiles.
 // Cap on persistent GEMM CTAs (0 = all SMs): overlap with a CTA-capped sync.
+// 1 (default): split-K the last partial wave into <= 8 pieces per tile;
+// n >= 2: at most n pieces; 0: whole tiles only.
+extern "C" int ntp_gemm_set_split_k(int on) {
+  if (on < 0 || on > 64) return fail(NTP_EINVAL, "split_k must be in [0, 64]");
+  gemm::g_split_k.store(on);
+  return NTP_OK;
+}
+
+// Debug hook, deliberately not in include/ntp_b200.h: device buffer of
+// gridDim * 16 * 8 u64 receiving per-item epilogue timestamps (nullptr: off).
+extern "C" int ntp_gemm_debug_trace(void *buf) {
+  gemm::g_trace = static_cast<unsigned long long *>(buf);
+  return NTP_OK;
+}
+
 extern "C" int ntp_gemm_set_max_ctas(int n) {
   if (n < 0) return fail(NTP_EINVAL, "bad CTA cap");
   gemm::g_max_ctas.store(n);

@@ -340,7 +340,6 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
 
 constexpr int kBulkConsumers = 128;                 // 4 consumer warps
 constexpr int kBulkThreads = kBulkConsumers + 32;   // + 1 producer warp
-constexpr int kChunkBytes = kChunkVecs * 16;        // 16 KiB per side per stage
 
 template <int kStages>
 struct BulkSmem {

@@ -64,6 +64,9 @@ def main():
             for mode, name_m in ((0, "single_256"), (2, "pair_128"), (3, "pair_256"), (1, "auto")):
                 _lib.load().ntp_gemm_set_pair(mode)
                 modes[name_m] = timed(ours)
+            _lib.load().ntp_gemm_set_split_k(0)
+            modes["auto_nosplit"] = timed(ours)
+            _lib.load().ntp_gemm_set_split_k(1)
             ms1 = modes["single_256"]
             ms = modes["auto"]
             ms_ref = timed(ref)

@@ -83,6 +83,52 @@ def test_gemm_epilogues_and_pitch(Lin):
     assert rel(arena[:, 1, :], acc) < 1e-5 and arena[:, 0, :].abs().max().item() == 0.0
 
 
+@pytest.mark.parametrize("M,N,K,a_mn,b_mn", [(3584, 4096, 8192, 1, 1),   # wgrad shape: 112 tiles
+                                             (1366, 1024, 4000, 0, 0),   # ragged M and K
+                                             (512, 2560, 2048, 1, 0)])
+def test_gemm_split_k_tail(Lin, M, N, K, a_mn, b_mn):
+    """The split-K tail (ntp_gemm_set_split_k) reproduces the whole-tile result
+    for every epilogue: partials are summed in piece order, so repeated runs are
+    bitwise identical, and the two schedules agree to fp32 rounding."""
+    from paper_2504_06095_b200 import _lib
+    L = _lib.load()
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = _mk(M, K, a_mn, g)
+    B = _mk(N, K, b_mn, g)
+    acc = A.float() @ B.float().T
+    res = {}
+    try:
+        for on in (1, 0):
+            L.ntp_gemm_set_split_k(on)
+            out = torch.empty((M, N), dtype=torch.float32, device="cuda")
+            Lin.mm(A, B, out)
+            again = torch.empty_like(out)
+            Lin.mm(A, B, again)
+            torch.cuda.synchronize()
+            assert torch.equal(out, again)
+            assert rel(out, acc) < 1e-5
+            H = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+            Y = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+            Lin.mm(A, B, Y, epilogue="gelu", aux=H)
+            D = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+            Lin.mm(A, B, D, epilogue="dgelu", aux=H)
+            # fused red epilogue: the local copy and a "partner" copy both get alpha*acc
+            loc = torch.zeros((M, N), dtype=torch.float32, device="cuda")
+            far = torch.zeros((M, N), dtype=torch.float32, device="cuda")
+            rb = torch.zeros(M, dtype=torch.int32, device="cuda")
+            rr = torch.arange(M, dtype=torch.int32, device="cuda")
+            Lin.mm_red(A, B, loc, 0.5, rb, rr, [far.data_ptr()], N)
+            torch.cuda.synchronize()
+            assert rel(loc, 0.5 * acc) < 1e-5 and rel(far, 0.5 * acc) < 1e-5
+            res[on] = (out, H, Y, D)
+    finally:
+        L.ntp_gemm_set_split_k(1)
+    assert rel(res[1][0], res[0][0]) < 2e-5  # different fp32 summation order
+    for a, b in zip(res[1][1:], res[0][1:]):
+        assert rel(a.float(), b.float()) < 1e-2
+    assert rel(res[1][1].float(), acc) < 5e-3
+
+
 def test_tp_mlp_forward_backward_vs_oracle(Lin):
     """TP4 comp layout of (1000, 4, 3): ragged, non-contiguous shards."""
     from paper_2504_06095_b200 import tpnumerics as T
