@@ -4,7 +4,8 @@ Rank 1 maps rank 0's buffer through CUDA IPC and times, per kernel variant:
   read  : local <- peer      (ntp_reshard, a = peer, b = local)
   write : peer  <- local     (ntp_reshard, a = local, b = peer)
   pair  : both <- w_a*peer + w_b*local   (ntp_grad_sync: read + write over the link)
-and a symmetric split where both ranks push half of the pair work at once.
+and a symmetric split where both ranks push half of the pair work at once,
+plus symmetric pure reads / writes (both ranks move the whole buffer at once).
 GB/s are per link direction.
 """
 
@@ -61,6 +62,8 @@ def main():
         return p.finalize().upload(local)
 
     bufs = [buf, peer]   # index 0 local, 1 peer
+    scratch = ops.alloc(nbytes)
+    bufs3 = [buf, peer, scratch]
     res = {}
     for vname, v in (("ldg", 1), ("bulk4x1", 2), ("bulk3x2", 3)):
         _lib.check(L.ntp_set_option(0, v))
@@ -82,6 +85,14 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         r["symmetric_pair_gbs_per_direction"] = round(nbytes / t.item() / 1e6, 1)
+        # symmetric read / write: both ranks move the whole buffer at once
+        for name, pl in (("symmetric_read_gbs_per_direction", plan(1, 2)),
+                         ("symmetric_write_gbs_per_direction", plan(2, 1))):
+            dist.barrier()
+            ms = timed(lambda: pl.reshard(bufs3))
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            r[name] = round(nbytes / t.item() / 1e6, 1)
         res[vname] = r
         dist.barrier()
     # reference: torch/NCCL send-recv of the same bytes (one direction)
@@ -107,6 +118,7 @@ def main():
     dist.barrier()
     ops.close(peer)
     ops.free(buf)
+    ops.free(scratch)
     dist.destroy_process_group()
 
 
