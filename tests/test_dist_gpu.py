@@ -66,3 +66,10 @@ def test_eight_gpus_c3():
 def test_fused_wgrad_sync_multi_gpu(n, n1, n2):
     """tcgen05 wgrad epilogues red.add into the partner replica over NVLink."""
     _run_script(n, "fused_check.py", n1, n2)
+
+
+@pytest.mark.parametrize("n,n1,dead", [(1, 4, 3), (2, 4, 1), (4, 2, 0)])
+def test_failure_reconfig_multi_gpu(n, n1, dead):
+    """dist_reconfig: H -> comp layout, D's survivors -> TP-(n1-1), the dead
+    rank's units pulled from H over NVLink; bit-exact for bf16 and fp32 state."""
+    _run_script(n, "reconfig_check.py", "check", n1, dead)
