@@ -234,8 +234,10 @@ def run_e2e_single(args, lay, plan, dtype, eb):
     from paper_2504_06095_b200.hostsync import HostSync
     from paper_2504_06095_b200.workloads import layer_pieces
     lpp = int(os.environ.get("NTP_E2E_LAYERS_PER_PIECE", "1"))
+    spp = int(os.environ.get("NTP_E2E_SEGS_PER_PIECE", "0")) or None
     hs = HostSync(plan, [e for e in lay.h_elems + lay.r_elems], dtype, device=0,
-                  piece_plans=layer_pieces(lay, dtype, 0, layers_per_piece=lpp))
+                  piece_plans=layer_pieces(lay, dtype, 0, layers_per_piece=lpp,
+                                           segs_per_piece=spp))
     gen = torch.Generator().manual_seed(1)
     host = [torch.randn(e, generator=gen, dtype=torch.float32).to(dtype).pin_memory()
             for e in lay.h_elems + lay.r_elems]
@@ -247,6 +249,30 @@ def run_e2e_single(args, lay, plan, dtype, eb):
     s1.record()
     torch.cuda.synchronize()
     h2d_gbs = sum(h.numel() for h in host) * eb / (s0.elapsed_time(s1) * 1e-3) / 1e9
+    # and both directions at once (what a pipelined step needs): 1 GiB each way
+    # on two streams, between device scratch and pinned host scratch
+    n = 1 << 30
+    hs_in = torch.empty(n, dtype=torch.uint8).pin_memory()
+    hs_out = torch.empty(n, dtype=torch.uint8).pin_memory()
+    dv = torch.empty(2 * n, dtype=torch.uint8, device="cuda")
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    best = float("inf")
+    for _ in range(4):  # first pass warms the pinned pages; best of the rest
+        torch.cuda.synchronize()
+        s0.record()
+        sa.wait_stream(torch.cuda.current_stream())
+        sb.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(sa):
+            dv[:n].copy_(hs_in, non_blocking=True)
+        with torch.cuda.stream(sb):
+            hs_out.copy_(dv[n:], non_blocking=True)
+        torch.cuda.current_stream().wait_stream(sa)
+        torch.cuda.current_stream().wait_stream(sb)
+        s1.record()
+        torch.cuda.synchronize()
+        best = min(best, s0.elapsed_time(s1))
+    duplex_gbs = n / (best * 1e-3) / 1e9
+    del hs_in, hs_out, dv
     steps = max(2, min(args.e2e_steps, args.steps))
     for _ in range(2):
         hs.run(host, W_H, W_R)
@@ -267,7 +293,9 @@ def run_e2e_single(args, lay, plan, dtype, eb):
             "gpu_launches_per_step": hs.launches_per_run,
             "pipeline_pieces": len(hs.pieces or []),
             "host_link_h2d_only_gbs": round(h2d_gbs, 1),
-            "host_link_bound_ms": round(nbytes / (h2d_gbs * 1e9) * 1e3, 2)}
+            "host_link_duplex_gbs_per_direction": round(duplex_gbs, 1),
+            "host_link_bound_ms": round(nbytes / (duplex_gbs * 1e9) * 1e3, 2),
+            "host_link_frac": round(nbytes / (duplex_gbs * 1e9) * 1e3 / ms, 3)}
 
 
 def _ncu_traffic():

@@ -110,13 +110,19 @@ def busiest_bytes(lay: PairLayout, elem_bytes: int) -> int:
     return max(max(lay.h_elems), max(lay.r_elems)) * elem_bytes
 
 
-def layer_pieces(lay: PairLayout, dtype, device: int, layers_per_piece: int = 1):
-    """Per-layer plans + the arena element ranges each touches (HostSync pieces)."""
+def layer_pieces(lay: PairLayout, dtype, device: int, layers_per_piece: int = 1,
+                 segs_per_piece: int | None = None):
+    """Per-layer (or per-segment: segs_per_piece=1 splits a layer into its MLP
+    and attention parts) plans + the arena element ranges each touches
+    (HostSync pieces).  Segments are contiguous in every arena, so a piece is
+    one element range per arena."""
     nseg = len(lay.shape.segments())
+    step = segs_per_piece if segs_per_piece else nseg * layers_per_piece
     pieces = []
     n1 = lay.n1
-    for l0 in range(0, lay.layers, layers_per_piece):
-        idx = range(l0 * nseg, min(lay.layers, l0 + layers_per_piece) * nseg)
+    total = lay.layers * nseg
+    for s0 in range(0, total, step):
+        idx = range(s0, min(total, s0 + step))
         plan = build_plan(lay, dtype, seg_filter=lambda i, s=idx: i in s).upload(device)
         ranges = []
         for side, count in ((0, n1), (1, lay.n2)):
