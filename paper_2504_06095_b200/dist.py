@@ -80,7 +80,7 @@ class Placement:
         return self.h_proc[slot] if slot < self.n1 else self.r_proc[slot - self.n1]
 
 
-def unit_executors(lay: PairLayout, plc: Placement, policy: str = "split"):
+def unit_executors(lay: PairLayout, plc: Placement, policy: str = "split", seg_filter=None):
     """Per segment: (h_owner, h_off, r_owner, r_off, executor_proc) arrays over
     the k units.  Units whose two owners share a process run there.  Otherwise
     ``policy`` decides which endpoint computes the unit:
@@ -95,7 +95,9 @@ def unit_executors(lay: PairLayout, plc: Placement, policy: str = "split"):
     out = []
     hp_of = np.asarray(plc.h_proc)
     rp_of = np.asarray(plc.r_proc)
-    for k, unit, hc, rc, hb, rb in lay.segs:
+    for si, (k, unit, hc, rc, hb, rb) in enumerate(lay.segs):
+        if seg_filter is not None and not seg_filter(si):
+            continue
         h_owner = np.empty(k, dtype=np.int64)
         h_off = np.empty(k, dtype=np.int64)
         r_owner = np.empty(k, dtype=np.int64)
@@ -119,12 +121,14 @@ def unit_executors(lay: PairLayout, plc: Placement, policy: str = "split"):
     return out
 
 
-def process_plan_units(lay: PairLayout, plc: Placement, rank: int, policy: str = "split"):
+def process_plan_units(lay: PairLayout, plc: Placement, rank: int, policy: str = "split",
+                       seg_filter=None):
     """The units `rank` computes, as per-segment (unit, h_slot, h_off, r_slot,
-    r_off) arrays in global slot numbering, plus the set of slots it touches."""
+    r_off) arrays in global slot numbering, plus the set of slots it touches.
+    seg_filter(i): restrict to some segments (a pipelined piece)."""
     out = []
     touched = set()
-    for unit, h_owner, h_off, r_owner, r_off, ex in unit_executors(lay, plc, policy):
+    for unit, h_owner, h_off, r_owner, r_off, ex in unit_executors(lay, plc, policy, seg_filter):
         sel = np.flatnonzero(ex == rank)
         if len(sel) == 0:
             continue
@@ -205,7 +209,16 @@ class NtpSyncGroup:
     """One process's share of a distributed nonuniform gradient sync."""
 
     def __init__(self, lay: PairLayout, placement: Placement, dtype: torch.dtype, device: int,
-                 ops: DeviceOps | None = None, group=None, policy: str = "split"):
+                 ops: DeviceOps | None = None, group=None, policy: str = "split",
+                 pieces=None):
+        """pieces: optional list of segment-index lists.  Each piece gets its
+        own plan, so a caller can sync piece i as soon as its gradients (or its
+        host-to-device copies) are in place: ``step(..., piece=i)``.  Every
+        process must step the pieces in the same order (epochs pair up)."""
+        self.pieces = [sorted(int(i) for i in p) for p in pieces] if pieces else []
+        for p in self.pieces:
+            if not p or p != list(range(p[0], p[-1] + 1)):
+                raise ValueError("a piece must be a non-empty contiguous range of segments")
         self.lay, self.plc, self.dtype, self.policy = lay, placement, dtype, policy
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
@@ -239,15 +252,29 @@ class NtpSyncGroup:
         self.buf_index = {s: i for i, s in enumerate(order)}
         self.bufs = [self.slot_ptr[s] for s in order]
         self.plan = None
+        remap = np.full(placement.n1 + placement.n2, -1, dtype=np.int64)
+        for s, i in self.buf_index.items():
+            remap[s] = i
         if units:
-            remap = np.full(placement.n1 + placement.n2, -1, dtype=np.int64)
-            for s, i in self.buf_index.items():
-                remap[s] = i
             plan = Plan(dtype_code(dtype))
             for unit, hs, ho, rs, ro in units:
                 plan.add_units(unit, remap[hs], ho, remap[rs], ro)
             self.plan = plan.finalize()
         self.units = sum(len(u[1]) for u in units)
+        self.piece_plans = []
+        for seg_ids in self.pieces:
+            sel = set(seg_ids)
+            pu, ptouched = process_plan_units(lay, placement, self.rank, policy,
+                                              seg_filter=sel.__contains__)
+            if not pu:
+                self.piece_plans.append(None)
+                continue
+            if not ptouched <= set(self.buf_index):
+                raise RuntimeError("piece touches a slot the whole plan does not")  # pragma: no cover
+            pp = Plan(dtype_code(dtype))
+            for unit, hs, ho, rs, ro in pu:
+                pp.add_units(unit, remap[hs], ho, remap[rs], ro)
+            self.piece_plans.append(pp.finalize())
         # signal words (slot = writer's world rank in the receiver's page)
         self.post_ready = [self.peer_sig[p] + 8 * (READY * SIG_WORDS + self.rank)
                            for p in self.partners]
@@ -263,6 +290,9 @@ class NtpSyncGroup:
     def upload(self) -> "NtpSyncGroup":
         if self.plan is not None:
             self.plan.upload(self.device)
+        for pp in self.piece_plans:
+            if pp is not None:
+                pp.upload(self.device)
         self._status = torch.zeros(1, dtype=torch.int32, device=f"cuda:{self.device}")
         return self
 
@@ -270,9 +300,25 @@ class NtpSyncGroup:
         """Torch view of a hosted logical rank's gradient arena."""
         return _wrap(self.local[slot], self.slot_elems[slot], self.dtype, self.device)
 
-    def step(self, w_h: float, w_r: float, stream=None, spin_ns: int = 20_000_000_000) -> None:
-        """One synchronisation; stream-ordered on `stream` (default: current)."""
+    def piece_ranges(self, piece: int) -> dict:
+        """slot -> (lo, hi) element range of a hosted arena that piece `piece`
+        reads and writes (segments are contiguous in every arena)."""
+        seg_ids = sorted(self.pieces[piece])
+        out = {}
+        for slot in self.hosted:
+            side, idx = (0, slot) if slot < self.plc.n1 else (1, slot - self.plc.n1)
+            first, last = self.lay.segs[seg_ids[0]], self.lay.segs[seg_ids[-1]]
+            lo = int(first[4 + side][idx])
+            hi = int(last[4 + side][idx]) + len(last[2 + side][idx]) * last[1]
+            out[slot] = (lo, hi)
+        return out
+
+    def step(self, w_h: float, w_r: float, stream=None, spin_ns: int = 20_000_000_000,
+             piece: int | None = None) -> None:
+        """One synchronisation (of the whole layout, or of one piece); stream-
+        ordered on `stream` (default: current)."""
         L = _lib.load()
+        plan = self.plan if piece is None else self.piece_plans[piece]
         self.epoch += 1
         e = self.epoch
         s = torch.cuda.current_stream(self.device) if stream is None else stream
@@ -281,13 +327,13 @@ class NtpSyncGroup:
         if self.post_ready:
             _lib.check(L.ntp_signal_post(_lib.u64_ptr_array(self.post_ready), len(self.post_ready),
                                          e, sp), "ntp_signal_post")
-        if self.plan is not None:
+        if plan is not None:
             if self.partners:
-                self.plan.grad_sync_signaled(self.bufs, OPS["weighted"], w_h, w_r,
-                                             self.wait_ready, self.post_done, e, spin_ns,
-                                             self._status.data_ptr(), s)
+                plan.grad_sync_signaled(self.bufs, OPS["weighted"], w_h, w_r,
+                                        self.wait_ready, self.post_done, e, spin_ns,
+                                        self._status.data_ptr(), s)
             else:
-                self.plan.grad_sync(self.bufs, OPS["weighted"], w_h, w_r, s)
+                plan.grad_sync(self.bufs, OPS["weighted"], w_h, w_r, s)
         elif self.partners:
             # nothing to compute: wait until partners may be touched, then release them
             _lib.check(L.ntp_signal_wait(_lib.u64_ptr_array(self.wait_ready), len(self.wait_ready),

@@ -52,13 +52,26 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n1, n2, q):
+def _worker(rank, world, port, n1, n2, q, pieces=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     lay = pair_layout(SHAPE, n1, n2)
     plc = D.Placement.default(world, n1, n2)
-    g = D.NtpSyncGroup(lay, plc, torch.float32, device=0, ops=FakeOps(rank))
-    tab = g.plan.export() if g.plan is not None else np.zeros((0, 5), dtype=np.int64)
+    g = D.NtpSyncGroup(lay, plc, torch.float32, device=0, ops=FakeOps(rank), pieces=pieces)
+    if pieces:
+        # the piece plans together must do exactly the whole plan's work
+        parts = [p.export() for p in g.piece_plans if p is not None]
+        tab = np.concatenate(parts) if parts else np.zeros((0, 5), dtype=np.int64)
+        whole = g.plan.export() if g.plan is not None else np.zeros((0, 5), dtype=np.int64)
+        assert int(tab[:, 4].sum()) == int(whole[:, 4].sum())
+        rng = [g.piece_ranges(i) for i in range(len(pieces))]
+        for a, b in zip(rng, rng[1:]):  # pieces tile every hosted arena in order
+            for s in g.hosted:
+                assert a[s][1] == b[s][0]
+        for s in g.hosted:
+            assert rng[0][s][0] == 0 and rng[-1][s][1] == g.slot_elems[s]
+    else:
+        tab = g.plan.export() if g.plan is not None else np.zeros((0, 5), dtype=np.int64)
     slots = sorted(g.slot_ptr)
     q.put((rank, tab, slots, g.wait_ready, g.post_done, g.post_ready, g.wait_done,
            g.partners, g.sig))
@@ -66,11 +79,12 @@ def _worker(rank, world, port, n1, n2, q):
     dist.destroy_process_group()
 
 
-def _run_world(world, n1, n2):
+def _run_world(world, n1, n2, pieces=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n1, n2, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n1, n2, q, pieces))
+             for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=120) for _ in range(world)]
@@ -195,3 +209,16 @@ def test_busiest_bytes_accounting():
     assert b8 == max(lay.r_elems) * 2 == 838926336
     # 2 GPUs: every unit crosses the one link
     assert busiest_bytes_for(lay, D.Placement.default(2, 4, 3), 2) == lay.elems * 2
+
+
+def test_gloo_world2_per_layer_pieces():
+    """Pipelined pieces (one per layer): their plans replay to the oracle and
+    their arena ranges tile every hosted arena."""
+    nseg = len(SHAPE.segments())
+    pieces = [list(range(i * nseg, (i + 1) * nseg)) for i in range(SHAPE.layers)]
+    per_rank = _run_world(2, 4, 3, pieces)
+    _replay(pair_layout(SHAPE, 4, 3), per_rank)
+    lay = pair_layout(SHAPE, 4, 3)
+    with pytest.raises(ValueError, match="contiguous range"):
+        D.NtpSyncGroup(lay, D.Placement.default(1, 4, 3), torch.float32, 0, ops=FakeOps(0),
+                       pieces=[[0, 2]])
