@@ -165,6 +165,16 @@ struct Params {
   // debug only (ntp_gemm_debug_trace): per (CTA, local item) 8 u64:
   // {item, t_full, t_done, t_kernel_start, t_prod_first, t_prod_last, t_mma_first, t_mma_last}
   unsigned long long *trace;
+  // EPI_PUSH with push_tma = 1: a 32-row box whose rows map to consecutive rows
+  // of one peer copy goes there as one TMA tensor store (peer_maps[pb]) from the
+  // same smem staging as the local store; other boxes fall back to row stores
+  int push_tma;
+};
+
+// Tensor maps over the peer copies (EPI_PUSH, push_tma): boxes of 32 x 32 at
+// the GEMM output's element type, row pitch red_ld.
+struct PeerMaps {
+  CUtensorMap m[kMaxPeers];
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -328,7 +338,7 @@ template <int BN, int kPair, int kStg>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
             const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_h,
-            Params p) {
+            const __grid_constant__ PeerMaps peer_maps, Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t base = smem_u32(smem_raw);
   unsigned char *aligned = smem_raw + ((1024u - (base & 1023u)) & 1023u);
@@ -465,7 +475,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         if (col0 >= p.N || row0 >= p.M) return;  // warp-uniform: nothing of this box is stored
 #pragma unroll
         for (int j = 0; j < 32; ++j) f[j] *= p.alpha;
-        if (p.epi == EPI_RED || p.epi == EPI_PUSH) {
+        if (p.epi == EPI_RED || (p.epi == EPI_PUSH && !p.push_tma)) {
           // fused sync: this replica's weighted contribution goes into its own copy
           // and, over NVLink, into the partner replica's copy (EPI_RED: red.add
           // into zeroed arenas) or the partner's staging arena (EPI_PUSH: plain
@@ -553,9 +563,26 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
+        // EPI_PUSH (TMA): the box also goes to the partner replica's staging copy
+        // -- one TMA store over NVLink when its 32 rows are consecutive rows of
+        // one peer copy, else row stores from registers (run boundaries, ragged M)
+        int peer_box = -1, peer_row0 = 0;
+        if (p.epi == EPI_PUSH) {
+          const int pb = row < p.M ? p.red_buf[row] : -1;
+          const int pr = row < p.M ? p.red_row[row] : 0;
+          const int pb0 = __shfl_sync(0xffffffffu, pb, 0), pr0 = __shfl_sync(0xffffffffu, pr, 0);
+          if (__all_sync(0xffffffffu, pb == pb0 && pb0 >= 0 && pr == pr0 + lane)) {
+            peer_box = pb0;
+            peer_row0 = pr0;
+          } else if (pb >= 0 && col0 + 32 <= p.N) {
+            const int ce = p.c_f32 ? 4 : 2;
+            store_row32(p.red_base[pb] + ((long long)pr * p.red_ld + col0) * ce, f, p.c_f32);
+          }
+        }
         if (lane == 0) {
           if (p.c_tma) tma_store_2d(&map_c, stage, col0, row0);  // TMA clips rows >= M, cols >= N
           if (p.epi == EPI_GELU && p.h_tma) tma_store_2d(&map_h, stage + 2048, col0, row0);
+          if (peer_box >= 0) tma_store_2d(&peer_maps.m[peer_box], stage, col0, peer_row0);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
         if (!p.c_tma) box_store(stage, p.C, p.ldc, p.c_f32 ? 4 : 2, row0, col0, p.M, p.N, lane);
@@ -817,7 +844,18 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
   p.H = H;
   p.ldc = ldc;
   p.ldh = ldh;
-  p.c_tma = p.epi != EPI_RED && p.epi != EPI_PUSH &&
+  PeerMaps pm;
+  memset(&pm, 0, sizeof pm);
+  if (p.epi == EPI_PUSH && p.push_tma) {
+    // rows: any row a box is checked to own (red_row) -- the extent only bounds the map
+    for (int i = 0; i < kMaxPeers && p.push_tma; ++i)
+      if (p.red_base[i] &&
+          make_map(&pm.m[i], p.red_base[i],
+                   p.c_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : BF, ce, p.N, 1ll << 24, p.red_ld,
+                   32, 32, NOSW))
+        p.push_tma = 0;  // unaligned peer copy: row stores only
+  }
+  p.c_tma = p.epi != EPI_RED && (p.epi != EPI_PUSH || p.push_tma) &&
             !((reinterpret_cast<uintptr_t>(C) & 15u) || ((ldc * ce) & 15));
   p.h_tma = p.epi == EPI_GELU && !((reinterpret_cast<uintptr_t>(H) & 15u) || ((ldh * 2) & 15));
   memset(&mc, 0, sizeof mc);
@@ -886,7 +924,7 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mh, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mh, pm, p);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(NTP_ECUDA, std::string("gemm launch: ") + cudaGetErrorString(e));
   return NTP_OK;
@@ -929,7 +967,8 @@ extern "C" int ntp_gemm_bf16_red(const void *A, int64_t lda, int a_mn, const voi
                                  const int32_t *red_buf, const int32_t *red_row,
                                  void *const *red_base, int n_red, int64_t red_ld, int mode,
                                  void *stream) {
-  if (mode != 0 && mode != 1) return fail(NTP_EINVAL, "fused mode must be 0 (red) or 1 (push)");
+  if (mode < 0 || mode > 2)
+    return fail(NTP_EINVAL, "fused mode must be 0 (red), 1 (push) or 2 (push, TMA boxes)");
   if (M <= 0 || N <= 0 || K <= 0) return fail(NTP_EINVAL, "GEMM extents must be positive");
   if (N % 32) return fail(NTP_EINVAL, "fused sync GEMM needs N % 32 == 0");
   if (n_red < 0 || n_red > gemm::kMaxPeers) return fail(NTP_EINVAL, "at most 8 peer copies");
@@ -948,6 +987,7 @@ extern "C" int ntp_gemm_bf16_red(const void *A, int64_t lda, int a_mn, const voi
     if (reinterpret_cast<uintptr_t>(p.red_base[i]) & 15u)
       return fail(NTP_EINVAL, "peer copies must be 16-byte aligned");
   p.red_ld = red_ld;
+  p.push_tma = mode == 2;
   return gemm::dispatch(A, lda, a_mn, B, ldb, b_mn, C, ldc, nullptr, 0, p,
                         static_cast<cudaStream_t>(stream));
 }
@@ -985,8 +1025,6 @@ int dispatch(const void *A, long long lda, int a_mn, const void *B, long long ld
 }  // namespace gemm
 }  // namespace ntp
 
-// 1 (default): 256-row CTA-pair tiles (tcgen05 cta_group::2) for N > 128; 0: 1-SM tiles.
-// Cap on persistent GEMM CTAs (0 = all SMs): overlap with a CTA-capped sync.
 // 1 (default): split-K the last partial wave into <= 8 pieces per tile;
 // n >= 2: at most n pieces; 0: whole tiles only.
 extern "C" int ntp_gemm_set_split_k(int on) {
@@ -1002,12 +1040,15 @@ extern "C" int ntp_gemm_debug_trace(void *buf) {
   return NTP_OK;
 }
 
+// Cap on persistent GEMM CTAs (0 = all SMs): overlap with a CTA-capped sync.
 extern "C" int ntp_gemm_set_max_ctas(int n) {
   if (n < 0) return fail(NTP_EINVAL, "bad CTA cap");
   gemm::g_max_ctas.store(n);
   return NTP_OK;
 }
 
+// 1 (default): CTA-pair tiles (tcgen05 cta_group::2), width picked per shape;
+// 0: 1-SM tiles; 2 / 3: force 256x128 / 256x256 pair tiles.
 extern "C" int ntp_gemm_set_pair(int mode) {
   if (mode < 0 || mode > 3) return fail(NTP_EINVAL, "pair mode must be 0..3");
   gemm::g_pair.store(mode);

@@ -72,6 +72,12 @@ def mm(A: torch.Tensor, Bt: torch.Tensor, out: torch.Tensor, *, epilogue: str = 
     return out
 
 
+# "red": red.add into zeroed arenas; "push": row stores into the partner's
+# staging arena; "push_tma": the same, but 32-row boxes whose rows are
+# consecutive in the partner's layout go as one TMA tensor store over NVLink
+FUSED_MODES = {"red": 0, "push": 1, "push_tma": 2}
+
+
 def mm_red(A: torch.Tensor, Bt: torch.Tensor, out: torch.Tensor, alpha: float,
            red_buf: torch.Tensor, red_row: torch.Tensor, red_bases, red_ld: int,
            stream=None, mode: str = "red") -> None:
@@ -79,7 +85,7 @@ def mm_red(A: torch.Tensor, Bt: torch.Tensor, out: torch.Tensor, alpha: float,
     (local copy) and into row red_row[m] of red_bases[red_buf[m]] (the partner's
     copy); both start at zero.  mode "push": plain stores into ``out`` and into
     the partner's staging arena.  red_buf/red_row: int32 device tensors [M]."""
-    if mode not in ("red", "push"):
+    if mode not in FUSED_MODES:
         raise ValueError(f"unknown fused mode {mode!r}")
     M, K = A.shape
     N, K2 = Bt.shape
@@ -96,7 +102,7 @@ def mm_red(A: torch.Tensor, Bt: torch.Tensor, out: torch.Tensor, alpha: float,
         ctypes.c_void_p(out.data_ptr()), out.stride(0), int(out.dtype == torch.float32),
         M, N, K, float(alpha), ctypes.c_void_p(red_buf.data_ptr()),
         ctypes.c_void_p(red_row.data_ptr()), _lib.ptr_array(red_bases), len(red_bases),
-        int(red_ld), 0 if mode == "red" else 1, ctypes.c_void_p(stream.cuda_stream)),
+        int(red_ld), FUSED_MODES[mode], ctypes.c_void_p(stream.cuda_stream)),
         "ntp_gemm_bf16_red")
 
 

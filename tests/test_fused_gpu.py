@@ -73,10 +73,13 @@ def test_fused_backward_sync_matches_unfused(mods, gdtype, tol):
     assert O.rel_err(dh[1], w_h * db1 + w_r * db2) < 2e-2
 
 
+@pytest.mark.parametrize("mode", ["push", "push_tma"])
 @pytest.mark.parametrize("gdtype,tol", [(torch.float32, 1e-5), (torch.bfloat16, 1e-2)])
-def test_fused_push_mode(mods, gdtype, tol):
+def test_fused_push_mode(mods, gdtype, tol, mode):
     """mode "push": plain stores into the partner's staging arena, then each
-    replica adds its staging locally -- same result, replicas bit-identical."""
+    replica adds its staging locally -- same result, replicas bit-identical.
+    "push_tma": 32-row boxes that are consecutive in the partner's layout go as
+    TMA tensor stores, the rest (run boundaries, ragged tails) as row stores."""
     Lin, T = mods
     from paper_2504_06095_b200.shardmap import build_shard_map
     h, k, tok_h, tok_r = 128, 600, 256, 192
@@ -102,10 +105,10 @@ def test_fused_push_mode(mods, gdtype, tol):
     sth, stf = T.MlpReplica(layer, hc, dtype=gdtype), T.MlpReplica(layer, rc, dtype=gdtype)
     for sh, cols, g in zip(sh_h, hc, fh.grads):
         rb, rr = Lin.partner_row_map(cols, rc, "cuda")
-        sh.backward_synced(bf(Xh).cuda(), bf(Gh).cuda(), g, w_h, rb, rr, stf.grads, mode="push")
+        sh.backward_synced(bf(Xh).cuda(), bf(Gh).cuda(), g, w_h, rb, rr, stf.grads, mode=mode)
     for sh, cols, g in zip(sh_r, rc, fr.grads):
         rb, rr = Lin.partner_row_map(cols, hc, "cuda")
-        sh.backward_synced(bf(Xr).cuda(), bf(Gr).cuda(), g, w_r, rb, rr, sth.grads, mode="push")
+        sh.backward_synced(bf(Xr).cuda(), bf(Gr).cuda(), g, w_r, rb, rr, sth.grads, mode=mode)
     for g, s in zip(fh.grads + fr.grads, sth.grads + stf.grads):
         Lin.finish_push(g, s)
     fh._has_grads = fr._has_grads = True
