@@ -90,7 +90,10 @@ def unit_executors(lay: PairLayout, plc: Placement, policy: str = "split", seg_f
       the second half on the healthy side -- both GPUs read and write over the
       link at once (measured: ~700 GB/s per direction vs ~495 GB/s when one
       side both reads and writes everything, profiles/r01_nvlink_probe.json);
-    * "reduced": every unit runs on its reduced owner's GPU (pure push).
+    * "reduced": every unit runs on its reduced owner's GPU (pure push);
+    * "healthy": every unit runs on its healthy owner's GPU -- the degraded
+      GPU, which already serves twice the units, does no sync work at all;
+    * a number x in [0, 1]: that share of each pair's units on the reduced side.
     """
     out = []
     hp_of = np.asarray(plc.h_proc)
@@ -110,15 +113,29 @@ def unit_executors(lay: PairLayout, plc: Placement, policy: str = "split", seg_f
             r_off[c] = rb[r] + np.arange(len(c)) * unit
         hp, rp = hp_of[h_owner], rp_of[r_owner]
         ex = rp.copy()
-        if policy == "split":
+        share = reduced_share(policy)
+        if share < 1.0:
             key = hp * (1 << 20) + rp
             for kv in np.unique(key[hp != rp]):
                 idx = np.flatnonzero(key == kv)
-                ex[idx[(len(idx) + 1) // 2:]] = hp[idx[0]]
-        elif policy != "reduced":
-            raise ValueError(f"unknown executor policy {policy!r}")
+                ex[idx[int(np.ceil(len(idx) * share)):]] = hp[idx[0]]
         out.append((unit, h_owner, h_off, r_owner, r_off, ex))
     return out
+
+
+def reduced_share(policy) -> float:
+    """Share of each (healthy GPU, reduced GPU) pair's units computed on the
+    reduced side under an executor policy."""
+    named = {"split": 0.5, "reduced": 1.0, "healthy": 0.0}
+    if policy in named:
+        return named[policy]
+    try:
+        x = float(policy)
+    except (TypeError, ValueError):
+        raise ValueError(f"unknown executor policy {policy!r}") from None
+    if not 0.0 <= x <= 1.0:
+        raise ValueError(f"executor share must be in [0, 1], got {x}")
+    return x
 
 
 def process_plan_units(lay: PairLayout, plc: Placement, rank: int, policy: str = "split",
@@ -237,26 +254,43 @@ class NtpSyncGroup:
         table = [None] * self.world
         dist.all_gather_object(table, mine, group=group)
         self.table = table
-        # 3. what this process computes, and which peer buffers it needs
-        units, touched = process_plan_units(lay, placement, self.rank, policy)
+        # 3. which partners this process hand-shakes with, then its plans
         self.partners = partners(lay, placement, self.rank)
         self.opened = {}
         self.slot_ptr = dict(self.local)
+        self.peer_sig = {p: self.ops.open(table[p]["sig"]) for p in self.partners}
+        self.plan = None
+        self.piece_plans = []
+        self._build_plans(policy)
+        # signal words (slot = writer's world rank in the receiver's page)
+        self.post_ready = [self.peer_sig[p] + 8 * (READY * SIG_WORDS + self.rank)
+                           for p in self.partners]
+        self.wait_ready = [self.sig + 8 * (READY * SIG_WORDS + p) for p in self.partners]
+        self.post_done = [self.peer_sig[p] + 8 * (DONE * SIG_WORDS + self.rank)
+                          for p in self.partners]
+        self.wait_done = [self.sig + 8 * (DONE * SIG_WORDS + p) for p in self.partners]
+        self.epoch = 0
+        self._status = None
+
+    def _build_plans(self, policy) -> None:
+        """What this process computes under an executor policy, which peer
+        buffers it needs (IPC-mapped on first use), and the plans over a dense
+        local buffer table (whole layout + one per piece)."""
+        lay, placement = self.lay, self.plc
+        units, touched = process_plan_units(lay, placement, self.rank, policy)
         for s in sorted(touched):
             if s not in self.slot_ptr:
                 proc = placement.proc_of_slot(s)
-                self.slot_ptr[s] = self.opened[s] = self.ops.open(table[proc]["slots"][s])
-        self.peer_sig = {p: self.ops.open(table[p]["sig"]) for p in self.partners}
-        # 4. the plan, with buffers renumbered to a dense local table
+                self.slot_ptr[s] = self.opened[s] = self.ops.open(self.table[proc]["slots"][s])
         order = sorted(self.slot_ptr)
         self.buf_index = {s: i for i, s in enumerate(order)}
         self.bufs = [self.slot_ptr[s] for s in order]
-        self.plan = None
         remap = np.full(placement.n1 + placement.n2, -1, dtype=np.int64)
         for s, i in self.buf_index.items():
             remap[s] = i
+        self.plan = None
         if units:
-            plan = Plan(dtype_code(dtype))
+            plan = Plan(dtype_code(self.dtype))
             for unit, hs, ho, rs, ro in units:
                 plan.add_units(unit, remap[hs], ho, remap[rs], ro)
             self.plan = plan.finalize()
@@ -271,19 +305,20 @@ class NtpSyncGroup:
                 continue
             if not ptouched <= set(self.buf_index):
                 raise RuntimeError("piece touches a slot the whole plan does not")  # pragma: no cover
-            pp = Plan(dtype_code(dtype))
+            pp = Plan(dtype_code(self.dtype))
             for unit, hs, ho, rs, ro in pu:
                 pp.add_units(unit, remap[hs], ho, remap[rs], ro)
             self.piece_plans.append(pp.finalize())
-        # signal words (slot = writer's world rank in the receiver's page)
-        self.post_ready = [self.peer_sig[p] + 8 * (READY * SIG_WORDS + self.rank)
-                           for p in self.partners]
-        self.wait_ready = [self.sig + 8 * (READY * SIG_WORDS + p) for p in self.partners]
-        self.post_done = [self.peer_sig[p] + 8 * (DONE * SIG_WORDS + self.rank)
-                          for p in self.partners]
-        self.wait_done = [self.sig + 8 * (DONE * SIG_WORDS + p) for p in self.partners]
-        self.epoch = 0
-        self._status = None
+        self.policy = policy
+
+    def set_policy(self, policy) -> "NtpSyncGroup":
+        """Rebuild the plans for another executor policy (same arenas, same
+        partners and signals); uploads them if the group was uploaded."""
+        reduced_share(policy)  # validate before touching anything
+        self._build_plans(policy)
+        if self._status is not None:
+            self.upload()
+        return self
 
     # -- device-side -----------------------------------------------------------
 

@@ -179,6 +179,11 @@ class Config:
         return {"gemm_done_ms": [round(t0.elapsed_time(e), 3) for e in g_end],
                 "sync_done_ms": [round(t0.elapsed_time(e), 3) for e in s_end]}
 
+    def set_policy(self, policy):
+        if self.groups[0].policy != policy:
+            for gr in self.groups:
+                gr.set_policy(policy)
+
     def describe(self):
         return {"n1": self.n1, "n2": self.n2, "tokens_healthy": self.tok_h,
                 "tokens_degraded": self.tok_r, "placement_healthy": list(self.plc.h_proc),
@@ -207,7 +212,8 @@ def timed(main, fn, iters):
 
 
 def modes(Lb, sms):
-    """name -> (setup(), run(cfg)).  setup sets the global kernel options."""
+    """name -> (setup(), run(cfg)[, executor policy]).  setup sets the global
+    kernel options; the policy (default "split") is applied to both configs."""
     def opts(kernel=0, cap=0, gemm_cap=0):
         def f():
             Lb.ntp_set_option(0, kernel)
@@ -224,6 +230,10 @@ def modes(Lb, sms):
         # register-staged sync (no smem) co-resides with the GEMM's 1 CTA/SM
         "overlap_ldg_cap148": (opts(1, 148), lambda c: c.backward(True)),
         "overlap_ldg_cap296": (opts(1, 296), lambda c: c.backward(True)),
+        # executor policy "healthy": the degraded GPU computes no sync units
+        "overlap_bulk_cap16_healthy": (opts(2, 16, sms - 16), lambda c: c.backward(True),
+                                       "healthy"),
+        "overlap_ldg_cap148_healthy": (opts(1, 148), lambda c: c.backward(True), "healthy"),
         "fused_red": (opts(), lambda c: c.fused_backward("red")),
         "fused_push": (opts(), lambda c: c.fused_backward("push")),
         "fused_push_tma": (opts(), lambda c: c.fused_backward("push_tma")),
@@ -259,10 +269,13 @@ def main():
     table = modes(Lb, sms)
     best = {name: [float("inf"), float("inf")] for name in table}
     for _ in range(args.rounds):
-        for name, (setup, run) in table.items():
+        for name, (setup, run, *pol) in table.items():
             setup()
             for j, cfg in enumerate((ntp, uni)):
+                cfg.set_policy(pol[0] if pol else "split")
                 best[name][j] = min(best[name][j], timed(main_s, lambda: run(cfg), args.iters))
+    for cfg in (ntp, uni):
+        cfg.set_policy("split")
     Lb.ntp_set_option(0, 1)
     Lb.ntp_set_option(1, 148)
     Lb.ntp_gemm_set_max_ctas(0)

@@ -222,3 +222,25 @@ def test_gloo_world2_per_layer_pieces():
     with pytest.raises(ValueError, match="contiguous range"):
         D.NtpSyncGroup(lay, D.Placement.default(1, 4, 3), torch.float32, 0, ops=FakeOps(0),
                        pieces=[[0, 2]])
+
+
+@pytest.mark.parametrize("policy", ["healthy", "0.25", 0.75])
+def test_executor_policies_cover_every_unit_once(policy):
+    """Any executor share: every unit computed by exactly one process, and the
+    union replays to the oracle; "healthy" leaves the degraded GPU idle."""
+    lay = pair_layout(SHAPE, 4, 3)
+    plc = D.Placement.default(2, 4, 3)
+    per_rank = {}
+    for rank in range(2):
+        units, _ = D.process_plan_units(lay, plc, rank, policy=policy)
+        rows = []
+        for unit, hs, ho, rs, ro in units:
+            rows += [(h, a, r, b, unit) for h, a, r, b in zip(hs, ho, rs, ro)]
+        per_rank[rank] = (np.array(rows, dtype=np.int64).reshape(-1, 5), list(range(7)))
+    _replay(lay, per_rank)
+    if policy == "healthy":
+        assert len(per_rank[1][0]) == 0  # GPU 1 hosts the reduced replica
+    with pytest.raises(ValueError, match="share must be in"):
+        D.reduced_share(1.5)
+    with pytest.raises(ValueError, match="unknown executor policy"):
+        D.reduced_share("nobody")
