@@ -222,6 +222,17 @@ int ntp_gemm_bf16(const void *A, int64_t lda, int a_mn, const void *B, int64_t l
                   void *C, int64_t ldc, int c_f32, int64_t M, int64_t N, int64_t K, int epilogue,
                   const void *aux, int64_t ld_aux, float alpha, void *stream);
 
+/* ntp_gemm_bf16 with an explicit programmatic-dependent-launch mode:
+ * pdl 0: ordinary stream order.  1: launched early; waits for the previous
+ * kernel of the stream before touching global memory, so its set-up overlaps
+ * that kernel's tail.  2: the caller guarantees this GEMM neither reads what
+ * the previous kernel writes nor writes what it reads or writes; it runs
+ * under the previous kernel's tail and does not complete before it. */
+int ntp_gemm_bf16_ex(const void *A, int64_t lda, int a_mn, const void *B, int64_t ldb, int b_mn,
+                     void *C, int64_t ldc, int c_f32, int64_t M, int64_t N, int64_t K,
+                     int epilogue, const void *aux, int64_t ld_aux, float alpha, int pdl,
+                     void *stream);
+
 /* Fused weight-gradient GEMM + NTP gradient sync: the epilogue adds
  * alpha * acc (this replica's batch-weighted gradient) with red.add into the
  * local row m of C AND into row red_row[m] of the partner replica's copy
@@ -234,7 +245,11 @@ int ntp_gemm_bf16(const void *A, int64_t lda, int a_mn, const void *B, int64_t l
  * mode 0: red.add into zeroed arenas as above.  mode 1 (push): plain stores of
  * the weighted tile into the local arena and into the partner's *staging*
  * arena (red_base); after the done handshake each side adds its staging into
- * its arena (ntp_grad_sync_ex with write mask 1) -- no remote atomics. */
+ * its arena (ntp_grad_sync_ex with write mask 1) -- no remote atomics.
+ * mode 2 (push, TMA): as mode 1, but each 32-row output box whose rows are
+ * consecutive rows of one partner copy is sent as one TMA tensor store over
+ * NVLink from the same shared-memory staging as the local store; other boxes
+ * (run boundaries, ragged tails) fall back to row stores. */
 int ntp_gemm_bf16_red(const void *A, int64_t lda, int a_mn, const void *B, int64_t ldb, int b_mn,
                       void *C, int64_t ldc, int c_f32, int64_t M, int64_t N, int64_t K,
                       float alpha, const int32_t *red_buf, const int32_t *red_row,
@@ -257,6 +272,10 @@ int ntp_gemm_set_max_ctas(int n);
  * n >= 2: at most n pieces per tile.  0: whole tiles only.  NTP_EINVAL
  * outside [0, 64]. */
 int ntp_gemm_set_split_k(int on);
+
+/* 1: every ntp_gemm_bf16 / ntp_gemm_bf16_red launch uses programmatic
+ * dependent launch mode 1 (see ntp_gemm_bf16_ex).  0 (default): off. */
+int ntp_gemm_set_pdl(int on);
 
 /* ------------------------------------------------------------------------
  * Multi-GPU plumbing: peer memory over NVLink/NVSwitch and device signals

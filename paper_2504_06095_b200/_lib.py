@@ -78,6 +78,11 @@ SIGNATURES = {
                                      ctypes.c_int, _vp, ctypes.c_int64, ctypes.c_int,
                                      ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                                      _vp, ctypes.c_int64, ctypes.c_float, _vp]),
+    "ntp_gemm_bf16_ex": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int, _vp, ctypes.c_int64,
+                                        ctypes.c_int, _vp, ctypes.c_int64, ctypes.c_int,
+                                        ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                        ctypes.c_int, _vp, ctypes.c_int64, ctypes.c_float,
+                                        ctypes.c_int, _vp]),
     "ntp_gemm_bf16_red": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int, _vp, ctypes.c_int64,
                                          ctypes.c_int, _vp, ctypes.c_int64, ctypes.c_int,
                                          ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
@@ -86,6 +91,7 @@ SIGNATURES = {
     "ntp_gemm_set_pair": (ctypes.c_int, [ctypes.c_int]),
     "ntp_gemm_set_max_ctas": (ctypes.c_int, [ctypes.c_int]),
     "ntp_gemm_set_split_k": (ctypes.c_int, [ctypes.c_int]),
+    "ntp_gemm_set_pdl": (ctypes.c_int, [ctypes.c_int]),
     "ntp_alloc": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, _vpp]),
     "ntp_free": (ctypes.c_int, [_vp]),
     "ntp_ipc_get_handle": (ctypes.c_int, [_vp, ctypes.c_char_p]),

@@ -169,6 +169,11 @@ struct Params {
   // of one peer copy goes there as one TMA tensor store (peer_maps[pb]) from the
   // same smem staging as the local store; other boxes fall back to row stores
   int push_tma;
+  // programmatic dependent launch: 0 off; 1 = wait for the previous kernel in
+  // the stream before touching global memory (prologue overlaps its tail);
+  // 2 = this GEMM's inputs and outputs are independent of the previous kernel
+  // (runs under its tail), but the grid does not complete before it does
+  int pdl;
 };
 
 // Tensor maps over the peer copies (EPI_PUSH, push_tma): boxes of 32 x 32 at
@@ -383,6 +388,12 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   if constexpr (kPair == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
+  if (p.pdl) {
+    // every CTA is resident (persistent grid): the next kernel may launch now
+    // and set up under this one's tail
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (p.pdl == 1) asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   if (p.trace && threadIdx.x == 0) p.trace[(size_t)blockIdx.x * kTraceItems * 8 + 3] = gtime();
 
   if (warp == 0) {
@@ -710,6 +721,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   }
   tc_fence_before();
   if constexpr (kPair == 2) cluster_sync(); else __syncthreads();
+  // independent GEMM (pdl 2): completes only after its predecessor, so a later
+  // kernel that waits on this one also sees the predecessor's results
+  if (p.pdl == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
   if (warp == 1) {
     tc_fence_after();
     if constexpr (kPair == 2)
@@ -780,6 +794,7 @@ static int sm_count_dev() {
 static std::atomic<int> g_pair{1};
 static std::atomic<int> g_max_ctas{0};
 static std::atomic<int> g_split_k{1};
+static std::atomic<int> g_pdl{0};
 static unsigned long long *g_trace = nullptr;
 
 // Split-K partials and per-slice arrival counters, one set per (device, stream)
@@ -812,16 +827,25 @@ struct Workspace {
   }
 };
 
+// A ring of 4 per stream: with programmatic dependent launch up to three
+// consecutive GEMMs of one stream can be in flight at once, and each launch
+// that splits K takes the next workspace of the ring.
+struct StreamWorkspaces {
+  Workspace w[4];
+  unsigned next = 0;
+};
+
 static Workspace &workspace_for(cudaStream_t s) {
   static std::mutex mu;
-  static std::vector<std::pair<std::pair<int, cudaStream_t>, Workspace *>> table;
+  static std::vector<std::pair<std::pair<int, cudaStream_t>, StreamWorkspaces *>> table;
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> g(mu);
   for (auto &e : table)
-    if (e.first.first == dev && e.first.second == s) return *e.second;
-  table.push_back({{dev, s}, new Workspace()});
-  return *table.back().second;
+    if (e.first.first == dev && e.first.second == s) return e.second->w[e.second->next++ & 3];
+  table.push_back({{dev, s}, new StreamWorkspaces()});
+  StreamWorkspaces *sw = table.back().second;
+  return sw->w[sw->next++ & 3];
 }
 
 template <int BN, int kPair, int kStg>
@@ -917,13 +941,15 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = kPair;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = p.pdl ? 2 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mh, pm, p);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(NTP_ECUDA, std::string("gemm launch: ") + cudaGetErrorString(e));
@@ -943,10 +969,24 @@ int dispatch(const void *A, long long lda, int a_mn, const void *B, long long ld
 
 using namespace ntp;
 
+extern "C" int ntp_gemm_bf16_ex(const void *A, int64_t lda, int a_mn, const void *B,
+                                int64_t ldb, int b_mn, void *C, int64_t ldc, int c_f32, int64_t M,
+                                int64_t N, int64_t K, int epilogue, const void *aux,
+                                int64_t ld_aux, float alpha, int pdl, void *stream);
+
 extern "C" int ntp_gemm_bf16(const void *A, int64_t lda, int a_mn, const void *B, int64_t ldb,
                              int b_mn, void *C, int64_t ldc, int c_f32, int64_t M, int64_t N,
                              int64_t K, int epilogue, const void *aux, int64_t ld_aux,
                              float alpha, void *stream) {
+  return ntp_gemm_bf16_ex(A, lda, a_mn, B, ldb, b_mn, C, ldc, c_f32, M, N, K, epilogue, aux,
+                          ld_aux, alpha, gemm::g_pdl.load(), stream);
+}
+
+extern "C" int ntp_gemm_bf16_ex(const void *A, int64_t lda, int a_mn, const void *B,
+                                int64_t ldb, int b_mn, void *C, int64_t ldc, int c_f32, int64_t M,
+                                int64_t N, int64_t K, int epilogue, const void *aux,
+                                int64_t ld_aux, float alpha, int pdl, void *stream) {
+  if (pdl < 0 || pdl > 2) return fail(NTP_EINVAL, "pdl must be 0, 1 (after) or 2 (independent)");
   if (M <= 0 || N <= 0 || K <= 0) return fail(NTP_EINVAL, "GEMM extents must be positive");
   if (M > (1ll << 31) || N > (1ll << 31) || K > (1ll << 31))
     return fail(NTP_EINVAL, "GEMM extent too large");
@@ -956,6 +996,7 @@ extern "C" int ntp_gemm_bf16(const void *A, int64_t lda, int a_mn, const void *B
   gemm::Params p{(int)M, (int)N, (int)K, a_mn ? 1 : 0, b_mn ? 1 : 0, c_f32 ? 1 : 0, epilogue,
                  static_cast<const __nv_bfloat16 *>(aux), ld_aux, alpha, 0, 0,
                  nullptr, nullptr, 0, 0, 0, 0};
+  p.pdl = pdl;
   return gemm::dispatch(A, lda, a_mn, B, ldb, b_mn, C, ldc, const_cast<void *>(aux), ld_aux, p,
                         static_cast<cudaStream_t>(stream));
 }
@@ -988,6 +1029,7 @@ extern "C" int ntp_gemm_bf16_red(const void *A, int64_t lda, int a_mn, const voi
       return fail(NTP_EINVAL, "peer copies must be 16-byte aligned");
   p.red_ld = red_ld;
   p.push_tma = mode == 2;
+  p.pdl = gemm::g_pdl.load();
   return gemm::dispatch(A, lda, a_mn, B, ldb, b_mn, C, ldc, nullptr, 0, p,
                         static_cast<cudaStream_t>(stream));
 }
@@ -1037,6 +1079,13 @@ extern "C" int ntp_gemm_set_split_k(int on) {
 // gridDim * 16 * 8 u64 receiving per-item epilogue timestamps (nullptr: off).
 extern "C" int ntp_gemm_debug_trace(void *buf) {
   gemm::g_trace = static_cast<unsigned long long *>(buf);
+  return NTP_OK;
+}
+
+// 1: every GEMM launch (ntp_gemm_bf16, ntp_gemm_bf16_red) uses programmatic
+// dependent launch, waiting for its predecessor before touching memory; 0: off.
+extern "C" int ntp_gemm_set_pdl(int on) {
+  gemm::g_pdl.store(on ? 1 : 0);
   return NTP_OK;
 }
 

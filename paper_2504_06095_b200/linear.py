@@ -41,12 +41,22 @@ def _operand(t: torch.Tensor):
     raise ValueError("GEMM operand must have a unit stride in one dimension")
 
 
+PDL = {None: -1, "off": 0, "after": 1, "independent": 2}
+
+
 def mm(A: torch.Tensor, Bt: torch.Tensor, out: torch.Tensor, *, epilogue: str = "none",
-       aux: torch.Tensor | None = None, alpha: float = 1.0, stream=None) -> torch.Tensor:
+       aux: torch.Tensor | None = None, alpha: float = 1.0, stream=None,
+       pdl: str | None = None) -> torch.Tensor:
     """out[M x N] = epilogue(A[M x K] @ Bt[N x K]^T) on the tensor cores.
 
     A and Bt may be K-major or MN-major views (e.g. ``Y.T``); ``out`` is a
-    row-major [M x N] view with any row pitch (bf16 or fp32)."""
+    row-major [M x N] view with any row pitch (bf16 or fp32).
+    pdl (programmatic dependent launch, ntp_gemm_bf16_ex): "after" overlaps
+    the launch's set-up with the previous kernel's tail; "independent" runs it
+    under that tail (the caller guarantees no data dependence either way);
+    None follows ntp_gemm_set_pdl."""
+    if pdl not in PDL:
+        raise ValueError(f"unknown pdl mode {pdl!r}")
     M, K = A.shape
     N, K2 = Bt.shape
     if K != K2 or tuple(out.shape) != (M, N):
@@ -64,11 +74,15 @@ def mm(A: torch.Tensor, Bt: torch.Tensor, out: torch.Tensor, *, epilogue: str = 
         aux_ptr, ld_aux = aux.data_ptr(), aux.stride(0)
     if stream is None:
         stream = torch.cuda.current_stream(A.device)
-    _lib.check(_lib.load().ntp_gemm_bf16(
-        ctypes.c_void_p(a_ptr), lda, a_mn, ctypes.c_void_p(b_ptr), ldb, b_mn,
-        ctypes.c_void_p(out.data_ptr()), out.stride(0), int(out.dtype == torch.float32),
-        M, N, K, EPI[epilogue], ctypes.c_void_p(aux_ptr), ld_aux, float(alpha),
-        ctypes.c_void_p(stream.cuda_stream)), "ntp_gemm_bf16")
+    L = _lib.load()
+    args = (ctypes.c_void_p(a_ptr), lda, a_mn, ctypes.c_void_p(b_ptr), ldb, b_mn,
+            ctypes.c_void_p(out.data_ptr()), out.stride(0), int(out.dtype == torch.float32),
+            M, N, K, EPI[epilogue], ctypes.c_void_p(aux_ptr), ld_aux, float(alpha))
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    if pdl is None:
+        _lib.check(L.ntp_gemm_bf16(*args, sp), "ntp_gemm_bf16")
+    else:
+        _lib.check(L.ntp_gemm_bf16_ex(*args, PDL[pdl], sp), "ntp_gemm_bf16_ex")
     return out
 
 
@@ -152,16 +166,29 @@ class MlpShard:
         else:
             mm(Y, self.W[:, 1, :].T, Z)
 
-    def backward(self, X: torch.Tensor, G: torch.Tensor, grads: torch.Tensor) -> None:
+    def backward(self, X: torch.Tensor, G: torch.Tensor, grads: torch.Tensor,
+                 pdl: str | None = None) -> None:
         """Weight gradients written unit-major into grads [n, 2, h] (bf16 or fp32):
-        grads[:, 1, :] = Y^T G, grads[:, 0, :] = D^T X with D = (G B_i^T) * GeLU'(H)."""
+        grads[:, 1, :] = Y^T G, grads[:, 0, :] = D^T X with D = (G B_i^T) * GeLU'(H).
+
+        pdl: chain the three GEMMs with programmatic dependent launch.  The
+        first GEMM takes this mode ("after", or "independent" when the caller
+        knows the previous kernel of the stream shares no data with it); dB,
+        which does not read D, runs "independent" under its tail; dA waits
+        ("after").  D is then a per-shard buffer, never a recycled temporary
+        a still-running GEMM could be reading."""
         T = X.shape[0]
         H, Y = self.H[:, :self.n], self.Y[:, :self.n]
-        Dfull = torch.empty((T, _pad8(self.n)), dtype=torch.bfloat16, device=X.device)
+        if pdl is None:
+            Dfull = torch.empty((T, _pad8(self.n)), dtype=torch.bfloat16, device=X.device)
+        else:
+            if getattr(self, "_D", None) is None or self._D.shape[0] != T:
+                self._D = torch.empty((T, _pad8(self.n)), dtype=torch.bfloat16, device=X.device)
+            Dfull = self._D
         D = Dfull[:, :self.n]
-        mm(G, self.W[:, 1, :], D, epilogue="dgelu", aux=H)
-        mm(Y.T, G.T, grads[:, 1, :])
-        mm(D.T, X.T, grads[:, 0, :])
+        mm(G, self.W[:, 1, :], D, epilogue="dgelu", aux=H, pdl=pdl)
+        mm(Y.T, G.T, grads[:, 1, :], pdl=None if pdl is None else "independent")
+        mm(D.T, X.T, grads[:, 0, :], pdl=None if pdl is None else "after")
 
     def backward_synced(self, X: torch.Tensor, G: torch.Tensor, grads: torch.Tensor, alpha: float,
                         red_buf: torch.Tensor, red_row: torch.Tensor, partner_arenas,

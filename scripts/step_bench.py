@@ -109,11 +109,13 @@ class Config:
             self.shards.append(per)
             self.fused.append(fper)
 
-    def backward(self, overlap: bool, sync: bool = True):
+    def backward(self, overlap: bool, sync: bool = True, pdl: bool = False):
         main, side = self.main, self.side
         for li in reversed(range(self.L)):
             for sh, X, G, grads in self.shards[li]:
-                sh.backward(X, G, grads)
+                # PDL chain: each layer's first GEMM shares no data with the
+                # previous layer's last one (G is given, D is per shard)
+                sh.backward(X, G, grads, pdl="independent" if pdl else None)
             if sync and overlap:
                 side.wait_stream(main)
                 self.groups[li].step(self.w_h, self.w_r, side)
@@ -222,6 +224,7 @@ def modes(Lb, sms):
         return f
     return {
         "backward": (opts(), lambda c: c.backward(False, sync=False)),
+        "backward_pdl": (opts(), lambda c: c.backward(False, sync=False, pdl=True)),
         "sync_only": (opts(), lambda c: c.sync_only()),
         "serial": (opts(), lambda c: c.backward(False)),
         # TMA-bulk sync (131 KB smem/CTA) cannot share an SM with a GEMM CTA:
@@ -234,6 +237,8 @@ def modes(Lb, sms):
         "overlap_bulk_cap16_healthy": (opts(2, 16, sms - 16), lambda c: c.backward(True),
                                        "healthy"),
         "overlap_ldg_cap148_healthy": (opts(1, 148), lambda c: c.backward(True), "healthy"),
+        "overlap_bulk_cap16_healthy_pdl": (opts(2, 16, sms - 16),
+                                           lambda c: c.backward(True, pdl=True), "healthy"),
         "fused_red": (opts(), lambda c: c.fused_backward("red")),
         "fused_push": (opts(), lambda c: c.fused_backward("push")),
         "fused_push_tma": (opts(), lambda c: c.fused_backward("push_tma")),
@@ -268,6 +273,10 @@ def main():
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     table = modes(Lb, sms)
     best = {name: [float("inf"), float("inf")] for name in table}
+    from bench import ClockSampler  # repo root is on sys.path
+    clocks = ClockSampler(local)
+    clocks.start()
+    clocks.mark("t0")
     for _ in range(args.rounds):
         for name, (setup, run, *pol) in table.items():
             setup()
@@ -276,6 +285,10 @@ def main():
                 best[name][j] = min(best[name][j], timed(main_s, lambda: run(cfg), args.iters))
     for cfg in (ntp, uni):
         cfg.set_policy("split")
+    clocks.mark("t1")
+    clk = clocks.stop()
+    all_clk = [None] * world
+    dist.all_gather_object(all_clk, clk)
     Lb.ntp_set_option(0, 1)
     Lb.ntp_set_option(1, 148)
     Lb.ntp_gemm_set_max_ctas(0)
@@ -303,6 +316,7 @@ def main():
         res["step_overhead_ntp_vs_uniform"] = round(best[bn][0] / best[bu][1] - 1.0, 4)
         res["exposed_sync_ms_ntp"] = round(best[bn][0] - best["backward"][0], 3)
         res["exposed_sync_ms_uniform"] = round(best[bu][1] - best["backward"][1], 3)
+        res["clocks_per_rank"] = all_clk
         res["timeline_ldg_cap148_per_rank"] = {"ntp": tls[0], "uniform": tls[1]}
         print(json.dumps(res, indent=1), flush=True)
     dist.barrier()

@@ -187,3 +187,41 @@ def test_tensor_core_grads_then_sync(Lin):
         da, db = rep.dense_grads()
         assert O.rel_err(da, da1 + da2) < 2e-2
         assert O.rel_err(db, db1 + db2) < 2e-2
+
+
+def test_pdl_chains_match_stream_order(Lin):
+    """Programmatic dependent launch (ntp_gemm_bf16_ex / MlpShard.backward(pdl=))
+    changes only when GEMMs start: a multi-layer backward chained with
+    "after"/"independent" launches gives the same bits as plain stream order,
+    and so does the global ntp_gemm_set_pdl switch."""
+    from paper_2504_06095_b200 import _lib
+    h, k, tok, layers = 256, 1366, 512, 4
+    rng = np.random.default_rng(7)
+    shards, inputs = [], []
+    for li in range(layers):
+        A, B = O.random_layer(h, k, seed=10 + li)
+        sh = Lin.MlpShard(A / np.sqrt(h), B / np.sqrt(k), np.arange(k))
+        X = torch.from_numpy(rng.standard_normal((tok, h))).to(torch.bfloat16).cuda()
+        G = torch.from_numpy(rng.standard_normal((tok, h))).to(torch.bfloat16).cuda()
+        sh.forward(X, torch.empty((tok, h), dtype=torch.float32, device="cuda"))
+        shards.append(sh)
+        inputs.append((X, G))
+
+    def run(pdl, global_pdl=0):
+        _lib.load().ntp_gemm_set_pdl(global_pdl)
+        try:
+            out = [torch.zeros((k, 2, h), dtype=torch.float32, device="cuda") for _ in range(layers)]
+            for li in reversed(range(layers)):
+                mode = None if pdl is None else ("independent" if li < layers - 1 else "after")
+                shards[li].backward(*inputs[li], out[li], pdl=mode)
+            torch.cuda.synchronize()
+            return out
+        finally:
+            _lib.load().ntp_gemm_set_pdl(0)
+
+    want = run(None)
+    for got in (run("chain"), run(None, global_pdl=1)):
+        for a, b in zip(got, want):
+            assert torch.equal(a, b)
+    with pytest.raises(ValueError, match="unknown pdl mode"):
+        Lin.mm(inputs[0][0], inputs[0][1], torch.empty((tok, tok), device="cuda"), pdl="soon")
