@@ -1,11 +1,14 @@
 """Multi-GPU parity of the fused wgrad GEMM + NTP sync (torchrun, >= 2 ranks).
 
-Every process runs its hosted shards' tcgen05 backward with the red.add
-epilogue into its own unit-major arena and the partner replica's (peer HBM);
-rank 0 gathers the arenas and compares the dense result with the fp64 oracle
-w_h * mlp_backward(X_h) + w_r * mlp_backward(X_r) (tpnumerics.py:220-235).
+Every process runs its hosted shards' tcgen05 backward with the fused sync
+epilogue: mode "red" red.adds into its own unit-major arena and the partner
+replica's (peer HBM); "push" / "push_tma" store into the partner's staging
+arena (row stores / TMA tensor stores over NVLink) and each side then adds its
+staging locally.  Rank 0 gathers the arenas and compares the dense result with
+the fp64 oracle w_h * mlp_backward(X_h) + w_r * mlp_backward(X_r)
+(tpnumerics.py:220-235); the two replicas' copies must be bit-identical.
 
-    torchrun --nproc-per-node N scripts/fused_check.py [n1 n2]
+    torchrun --nproc-per-node N scripts/fused_check.py [n1 n2 mode]
 """
 
 import os
@@ -19,7 +22,7 @@ import torch.distributed as dist  # noqa: E402
 
 from oracle import oracle as O  # noqa: E402
 from paper_2504_06095_b200.dist import NtpSyncGroup, Placement  # noqa: E402
-from paper_2504_06095_b200.linear import MlpShard, partner_row_map  # noqa: E402
+from paper_2504_06095_b200.linear import MlpShard, finish_push, partner_row_map  # noqa: E402
 from paper_2504_06095_b200.workloads import ModelShape, pair_layout  # noqa: E402
 
 
@@ -34,6 +37,7 @@ class _P:
 def main():
     n1 = int(sys.argv[1]) if len(sys.argv) > 1 else 2
     n2 = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    mode = sys.argv[3] if len(sys.argv) > 3 else "red"
     os.environ["NCCL_DEBUG"] = "WARN"
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -45,6 +49,7 @@ def main():
     lay = pair_layout(ModelShape("fused", h, k, 0, 1), n1, n2)
     plc = Placement.default(world, n1, n2)
     grp = NtpSyncGroup(lay, plc, torch.float32, local).upload()
+    stg = NtpSyncGroup(lay, plc, torch.float32, local).upload() if mode != "red" else None
     _, unit, hc, rc, _, _ = lay.segs[0]
     rng = np.random.default_rng(5)  # identical on every rank
     bf = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(torch.bfloat16)  # noqa: E731
@@ -60,19 +65,23 @@ def main():
         sh = MlpShard(A, B, cols)
         sh.forward(bf(X).cuda(), torch.empty((X.shape[0], h), device="cuda"))
         slots = [n1 + j for j in range(n2)] if healthy else list(range(n1))
-        ptrs = grp.open_slots(slots)
+        ptrs = (grp if mode == "red" else stg).open_slots(slots)
         rb, rr = partner_row_map(cols, rc if healthy else hc, "cuda")
         work.append((sh, bf(X).cuda(), bf(G).cuda(), grp.arena(s).view(len(cols), 2, h),
-                     w_h if healthy else w_r, rb, rr, ptrs))
+                     w_h if healthy else w_r, rb, rr, ptrs, s))
     e = 1
-    for s in grp.hosted:
-        grp.arena(s).zero_()
+    if mode == "red":
+        for s in grp.hosted:
+            grp.arena(s).zero_()
     grp.signal("post_ready", e)
     grp.signal("wait_ready", e)
-    for sh, X, G, grads, alpha, rb, rr, ptrs in work:
-        sh.backward_synced(X, G, grads, alpha, rb, rr, [_P(p) for p in ptrs])
+    for sh, X, G, grads, alpha, rb, rr, ptrs, _s in work:
+        sh.backward_synced(X, G, grads, alpha, rb, rr, [_P(p) for p in ptrs], mode=mode)
     grp.signal("post_done", e)
     grp.signal("wait_done", e)
+    if mode != "red":
+        for sh, X, G, grads, alpha, rb, rr, ptrs, s in work:
+            finish_push(grp.arena(s), stg.arena(s))
     torch.cuda.synchronize()
     dist.barrier()
     assert grp.status() == 0, "signal timeout"
@@ -98,9 +107,11 @@ def main():
                 dense.setdefault(int(c), []).append(u[p])
         same = all(np.array_equal(v[0], v[1]) for v in dense.values())
         ok = worst < 2e-2 and same
-        print(f"fused_check world={world} n1={n1} n2={n2} worst_rel_err={worst:.3e} "
+        print(f"fused_check {mode} world={world} n1={n1} n2={n2} worst_rel_err={worst:.3e} "
               f"replicas_identical={same} {'PASS' if ok else 'FAIL'}", flush=True)
     grp.close()
+    if stg is not None:
+        stg.close()
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)
 

@@ -62,10 +62,13 @@ def test_eight_gpus_c3():
     _run_script(8, "dp_check.py", 3, 2, 1, "bf16", 2)
 
 
-@pytest.mark.parametrize("n,n1,n2", [(2, 2, 1), (4, 2, 1)])
-def test_fused_wgrad_sync_multi_gpu(n, n1, n2):
-    """tcgen05 wgrad epilogues red.add into the partner replica over NVLink."""
-    _run_script(n, "fused_check.py", n1, n2)
+@pytest.mark.parametrize("mode", ["red", "push", "push_tma"])
+@pytest.mark.parametrize("n,n1,n2", [(2, 2, 1), (4, 2, 1), (2, 4, 3)])
+def test_fused_wgrad_sync_multi_gpu(n, n1, n2, mode):
+    """tcgen05 wgrad epilogues send this replica's weighted gradient to the
+    partner replica over NVLink: red.add, row-store push, or TMA-box push into
+    IPC-mapped staging, then the local add."""
+    _run_script(n, "fused_check.py", n1, n2, mode)
 
 
 @pytest.mark.parametrize("n,n1,dead", [(1, 4, 3), (2, 4, 1), (4, 2, 0)])
