@@ -249,23 +249,27 @@ def run_e2e_single(args, lay, plan, dtype, eb):
     s1.record()
     torch.cuda.synchronize()
     h2d_gbs = sum(h.numel() for h in host) * eb / (s0.elapsed_time(s1) * 1e-3) / 1e9
-    # and both directions at once (what a pipelined step needs): 1 GiB each way
-    # on two streams, between device scratch and pinned host scratch
-    n = 1 << 30
+    # and both directions at once (what a pipelined step needs): 2 GiB each way
+    # in 8 pieces per direction on two streams, like the pipeline's copies,
+    # between device scratch and pinned host scratch
+    n, pieces = 2 << 30, 8
     hs_in = torch.empty(n, dtype=torch.uint8).pin_memory()
     hs_out = torch.empty(n, dtype=torch.uint8).pin_memory()
     dv = torch.empty(2 * n, dtype=torch.uint8, device="cuda")
     sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    step = n // pieces
     best = float("inf")
     for _ in range(4):  # first pass warms the pinned pages; best of the rest
         torch.cuda.synchronize()
         s0.record()
         sa.wait_stream(torch.cuda.current_stream())
         sb.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(sa):
-            dv[:n].copy_(hs_in, non_blocking=True)
-        with torch.cuda.stream(sb):
-            hs_out.copy_(dv[n:], non_blocking=True)
+        for i in range(pieces):
+            lo, hi = i * step, (i + 1) * step
+            with torch.cuda.stream(sa):
+                dv[lo:hi].copy_(hs_in[lo:hi], non_blocking=True)
+            with torch.cuda.stream(sb):
+                hs_out[lo:hi].copy_(dv[n + lo:n + hi], non_blocking=True)
         torch.cuda.current_stream().wait_stream(sa)
         torch.cuda.current_stream().wait_stream(sb)
         s1.record()
