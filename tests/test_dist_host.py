@@ -244,3 +244,13 @@ def test_executor_policies_cover_every_unit_once(policy):
         D.reduced_share(1.5)
     with pytest.raises(ValueError, match="unknown executor policy"):
         D.reduced_share("nobody")
+
+
+def test_gloo_world8_pieces_idle_gpu():
+    """The 8-GPU bench with per-layer pieces: GPU 7 (the "failed" one) hosts no
+    arena and gets no piece plans; the rest replay to the oracle."""
+    nseg = len(SHAPE.segments())
+    pieces = [list(range(i * nseg, (i + 1) * nseg)) for i in range(SHAPE.layers)]
+    per_rank = _run_world(8, 4, 3, pieces)
+    _replay(pair_layout(SHAPE, 4, 3), per_rank)
+    assert len(per_rank[7][0]) == 0 and per_rank[7][6] == []
