@@ -2,7 +2,10 @@
 replicas + one degraded TP-n2 replica through dist_dp.NtpDpGroup, compared with
 the oracle's uniform_sync arithmetic on dense layouts.
 
-    torchrun --nproc-per-node 4 scripts/dp_check.py [m n1 n2 dtype steps]
+    torchrun --nproc-per-node 4 scripts/dp_check.py [m n1 n2 dtype steps pieces algo]
+
+algo "nccl" (default): fold-in / NCCL all-reduce / push-back (NtpDpGroup);
+"multi": one R-way peer-memory kernel per process (NtpDpMultiGroup).
 """
 
 import os
@@ -15,7 +18,7 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 from oracle import oracle as O  # noqa: E402
-from paper_2504_06095_b200.dist_dp import DpPlacement, NtpDpGroup  # noqa: E402
+from paper_2504_06095_b200.dist_dp import DpPlacement, NtpDpGroup, NtpDpMultiGroup  # noqa: E402
 
 DT = {"f32": torch.float32, "bf16": torch.bfloat16}
 TOL = {"f32": 1e-6, "bf16": 2e-2}
@@ -27,6 +30,8 @@ def main():
     n2 = int(sys.argv[3]) if len(sys.argv) > 3 else 1
     dname = sys.argv[4] if len(sys.argv) > 4 else "f32"
     steps = int(sys.argv[5]) if len(sys.argv) > 5 else 2
+    pieces = int(sys.argv[6]) if len(sys.argv) > 6 else 1
+    algo = sys.argv[7] if len(sys.argv) > 7 else "nccl"
     os.environ["NCCL_DEBUG"] = "WARN"
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -38,7 +43,10 @@ def main():
     batches = [n1] * m + [n2]  # local batch proportional to TP degree
     w = np.array(batches, dtype=np.float64) / sum(batches)
     plc = DpPlacement.default(world, m, n1, n2)
-    grp = NtpDpGroup(k, unit, m, plc, dtype, local, w).upload()
+    if algo == "multi":
+        grp = NtpDpMultiGroup(k, unit, m, plc, dtype, local, w).upload()
+    else:
+        grp = NtpDpGroup(k, unit, m, plc, dtype, local, w, pieces=pieces).upload()
     rng = np.random.default_rng(0)
     dense = [torch.from_numpy(rng.standard_normal((k, unit))).to(dtype).double().numpy()
              for _ in range(m + 1)]

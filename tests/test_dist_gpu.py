@@ -52,9 +52,19 @@ def _run_script(n, script, *args):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-def test_four_gpus_dp3_with_degraded_replica(dtype):
-    """DP=3: two healthy TP2 replicas (one GPU each) + a TP1 replica."""
-    _run_script(4, "dp_check.py", 2, 2, 1, dtype, 2)
+@pytest.mark.parametrize("pieces", [1, 5])
+def test_four_gpus_dp3_with_degraded_replica(dtype, pieces):
+    """DP=3: two healthy TP2 replicas (one GPU each) + a TP1 replica; pieces > 1
+    pipelines fold-in / NCCL all-reduce / push-back on three streams."""
+    _run_script(4, "dp_check.py", 2, 2, 1, dtype, 2, pieces)
+
+
+@pytest.mark.parametrize("pieces,algo", [(1, "nccl"), (4, "nccl"), (1, "multi")])
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_four_gpus_c3_shape(pieces, algo, dtype):
+    """BASELINE configs[2] shape on 4 GPUs: DP=4 (3 x TP2 + 1 x TP1), through
+    NCCL among the healthy replicas or one R-way peer-memory kernel."""
+    _run_script(4, "dp_check.py", 3, 2, 1, dtype, 2, pieces, algo)
 
 
 def test_eight_gpus_c3():
