@@ -51,9 +51,9 @@ def _run(world, m, n1, n2, pieces):
     return {o[0]: o[1:] for o in out}
 
 
-@pytest.mark.parametrize("m,pieces", [(2, 1), (2, 5), (3, 4)])
-def test_gloo_dp_plans_cover_degraded_units_once(m, pieces):
-    n1, n2, world = 2, 1, 4
+@pytest.mark.parametrize("world,m,pieces", [(4, 2, 1), (4, 2, 5), (4, 3, 4), (7, 3, 3)])
+def test_gloo_dp_plans_cover_degraded_units_once(world, m, pieces):
+    n1, n2 = 2, 1
     per = _run(world, m, n1, n2, pieces)
     d_slot0 = m * n1
     covered_d = np.zeros(K * UNIT, dtype=np.int32)  # the degraded (TP1) arena
