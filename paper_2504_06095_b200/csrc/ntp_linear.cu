@@ -162,6 +162,7 @@ struct Params {
   int full_items, split;
   int *tile_cnt;
   float *ws;
+  unsigned long long split_window_ns;  // how long a piece waits for the others
   // debug only (ntp_gemm_debug_trace): per (CTA, local item) 8 u64:
   // {item, t_full, t_done, t_kernel_start, t_prod_first, t_prod_last, t_mma_first, t_mma_last}
   unsigned long long *trace;
@@ -657,29 +658,37 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         }
       }
       if (slice) {
-        // Distributed fixup: the `split` pieces of this warp slice meet at a
-        // counter (all of them run in the final wave of this persistent grid),
-        // then piece i sums every partial, in piece order (deterministic), for
-        // the 32-column chunks i, i+split, ... and runs their epilogue.
+        // Fixup without a blocking barrier.  Every piece publishes its partial
+        // and arrives; a piece that sees all `split` pieces arrive within a
+        // short window sums every partial, in piece order (deterministic), for
+        // its own 32-column chunks i, i+split, ...; chunks are claimed
+        // atomically, and the last piece to arrive sums every chunk nobody has
+        // claimed.  Nothing waits for a piece that is not running, so the GEMM
+        // stays deadlock-free next to kernels that hold SMs; with all pieces
+        // co-resident (the normal case) the fixup work is spread over them.
+        // Slot layout per warp slice: [arrive, depart, claim[BN/32]].
+        constexpr int kSlot = 2 + BN / 32;
         __threadfence();
         __syncwarp();
-        int *cnt = p.tile_cnt + (((size_t)w.tail * kPair + rank) * 4 + q) * 2;
+        int *cnt = p.tile_cnt + (((size_t)w.tail * kPair + rank) * 4 + q) * kSlot;
+        int old = 0, arrived = 0;
         if (lane == 0) {
-          atomicAdd(cnt, 1);
+          old = atomicAdd(cnt, 1);
+          arrived = old + 1;
           const unsigned long long t0 = gtime();
-          for (;;) {
-            int n;
-            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(n) : "l"(cnt) : "memory");
-            if (n >= p.split) break;
-            if (gtime() - t0 > 4000000000ull) asm volatile("trap;");
+          while (arrived < p.split && gtime() - t0 < p.split_window_ns) {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(arrived) : "l"(cnt) : "memory");
           }
         }
-        __syncwarp();
+        old = __shfl_sync(0xffffffffu, old, 0);
+        arrived = __shfl_sync(0xffffffffu, arrived, 0);
         __threadfence();
         const size_t piece_stride = (size_t)kPair * BM * BN / 4;  // float4s
         const float4 *base = slice - (size_t)w.piece * piece_stride;
-#pragma unroll 1
-        for (int c = w.piece * 32; c < BN; c += 32 * p.split) {
+        auto fix = [&](const int c) {
+          int won = 0;
+          if (lane == 0) won = atomicExch(cnt + 2 + c / 32, 1) == 0;
+          if (!__shfl_sync(0xffffffffu, won, 0)) return;
           float f[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) f[j] = 0.0f;
@@ -707,12 +716,20 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             }
           }
           emit(n0, row0, c, f);
+        };
+        if (arrived >= p.split) {  // everyone published: my own chunks
+#pragma unroll 1
+          for (int c = w.piece * 32; c < BN; c += 32 * p.split) fix(c);
         }
-        // the last piece to leave resets both counters for the next launch
+        if (old == p.split - 1) {  // last arrival: every chunk still unclaimed
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 32) fix(c);
+        }
+        // the last piece to leave resets the slot for the next launch
         __syncwarp();
         if (lane == 0 && atomicAdd(cnt + 1, 1) == p.split - 1) {
-          cnt[0] = 0;
-          cnt[1] = 0;
+          __threadfence();
+          for (int t = 0; t < kSlot; ++t) cnt[t] = 0;
         }
       }
       if (tr) trp[2] = gtime();
@@ -796,6 +813,7 @@ static std::atomic<int> g_max_ctas{0};
 static std::atomic<int> g_split_k{1};
 static std::atomic<int> g_pdl{0};
 static unsigned long long *g_trace = nullptr;
+static std::atomic<unsigned long long> g_split_window_ns{250000};
 
 // Split-K partials and per-slice arrival counters, one set per (device, stream)
 // so GEMMs on different streams never share them.  Grow-only; counters are
@@ -911,6 +929,7 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
   p.tile_cnt = nullptr;
   p.ws = nullptr;
   p.trace = g_trace;
+  p.split_window_ns = g_split_window_ns.load();
   const int rem = tiles % units, nkb = (p.K + BK - 1) / BK;
   if (g_split_k.load() && rem > 0) {
     const int cap_s = g_split_k.load() >= 2 ? g_split_k.load() : 8;
@@ -920,7 +939,7 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
     if (S > BN / 32) S = BN / 32;      // every piece fixes up >= 1 column chunk
     Workspace &w = workspace_for(s);
     const size_t need_ws = (size_t)rem * S * kPair * BM * BN * sizeof(float);
-    const size_t need_cnt = (size_t)rem * kPair * 4 * 2 * sizeof(int);
+    const size_t need_cnt = (size_t)rem * kPair * 4 * (2 + BN / 32) * sizeof(int);
     cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(s, &cap_st);
     // never allocate inside a graph capture: run whole tiles instead
@@ -1077,6 +1096,14 @@ extern "C" int ntp_gemm_set_split_k(int on) {
 
 // Debug hook, deliberately not in include/ntp_b200.h: device buffer of
 // gridDim * 16 * 8 u64 receiving per-item epilogue timestamps (nullptr: off).
+// Debug hook, not in the header: how long a split-K piece waits for the other
+// pieces of its tile before leaving the fixup to the last arrival (default
+// 250 us; 0 forces the last-arrival path).
+extern "C" int ntp_gemm_debug_split_window(unsigned long long ns) {
+  gemm::g_split_window_ns.store(ns);
+  return NTP_OK;
+}
+
 extern "C" int ntp_gemm_debug_trace(void *buf) {
   gemm::g_trace = static_cast<unsigned long long *>(buf);
   return NTP_OK;

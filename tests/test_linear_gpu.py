@@ -124,6 +124,18 @@ def test_gemm_split_k_tail(Lin, M, N, K, a_mn, b_mn):
     finally:
         L.ntp_gemm_set_split_k(1)
     assert rel(res[1][0], res[0][0]) < 2e-5  # different fp32 summation order
+    # the last-arrival fixup path (no piece waits for the others) gives the same bits
+    import ctypes
+    fn = L.ntp_gemm_debug_split_window
+    fn.argtypes = [ctypes.c_ulonglong]
+    try:
+        fn(0)
+        out0 = torch.empty((M, N), dtype=torch.float32, device="cuda")
+        Lin.mm(A, B, out0)
+        torch.cuda.synchronize()
+    finally:
+        fn(250000)
+    assert torch.equal(out0, res[1][0])
     for a, b in zip(res[1][1:], res[0][1:]):
         assert rel(a.float(), b.float()) < 1e-2
     assert rel(res[1][1].float(), acc) < 5e-3
