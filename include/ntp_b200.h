@@ -267,8 +267,10 @@ int ntp_gemm_set_max_ctas(int n);
 
 /* 1 (default): when the persistent schedule ends in a partial wave of R tiles,
  * those tiles are split along K into up to 8 pieces run by idle CTA pairs; fp32
- * partials meet in a per-stream workspace and the last piece of each 32-row
- * slice sums them in piece order (deterministic) and runs the epilogue.
+ * partials meet in a per-stream workspace; the pieces share the final sums
+ * (in piece order, deterministic) and epilogues by atomically claimed column
+ * chunks, and the last piece to arrive takes every unclaimed chunk -- no piece
+ * ever waits for one that is not running.
  * n >= 2: at most n pieces per tile.  0: whole tiles only.  NTP_EINVAL
  * outside [0, 64]. */
 int ntp_gemm_set_split_k(int on);
