@@ -74,6 +74,7 @@ SIGNATURES = {
     "ntp_mplan_destroy": (None, [_vp]),
     "ntp_multi_sync": (ctypes.c_int, [_vp, _vpp, ctypes.c_int, ctypes.c_int,
                                       ctypes.POINTER(ctypes.c_double), _vp]),
+    "ntp_multi_set_kernel": (ctypes.c_int, [ctypes.c_int]),
     "ntp_gemm_bf16": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int, _vp, ctypes.c_int64,
                                      ctypes.c_int, _vp, ctypes.c_int64, ctypes.c_int,
                                      ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <new>
 #include <string>
@@ -125,6 +126,151 @@ multi_kernel(Table tab, int n_chunks, BufTable bufs, Weights wts, int op) {
     }
   }
 }
+
+// ---------------------------------------------------------------------------
+// TMA-bulk variant (R <= 4): a producer warp streams the R copies of each chunk
+// into a shared-memory ring with cp.async.bulk (mbarrier complete_tx), four
+// consumer warps combine them in place, and one thread bulk-stores the result
+// to all R owners.  Up to 192 KiB per SM in flight: with peer-mapped copies the
+// NVLink reads of the next chunks overlap the stores of this one.
+
+constexpr int kBulkConsumers = 128;
+constexpr int kBulkThreads = kBulkConsumers + 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+template <int R, int kStages>
+struct BulkSmem {
+  uint4 slot[kStages][R][kChunkVecs];
+  uint64_t full[kStages];
+  uint64_t empty[kStages];
+};
+
+template <typename T, int R, int kStages>
+__global__ void __launch_bounds__(kBulkThreads, 1)
+multi_kernel_bulk(Table tab, int n_chunks, BufTable bufs, Weights wts, int op) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  auto &sm = *reinterpret_cast<BulkSmem<R, kStages> *>(smem_raw);
+  constexpr int E = Vec<T>::n;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid >= kBulkConsumers) {
+    // ---- producer ----
+    if (tid == kBulkConsumers) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+        const uint32_t bytes = __ldg(tab.len + c) * 16u;
+        mbar_wait(&sm.empty[stage], phase ^ 1u);
+        mbar_expect_tx(&sm.full[stage], R * bytes);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const uint4 *src =
+              reinterpret_cast<const uint4 *>(bufs.p[__ldg(tab.buf[r] + c)]) + __ldg(tab.off[r] + c);
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_u32(sm.slot[stage][r])),
+              "l"(src), "r"(bytes), "r"(smem_u32(&sm.full[stage]))
+              : "memory");
+        }
+        if (++stage == kStages) { stage = 0; phase ^= 1u; }
+      }
+    }
+    return;
+  }
+  // ---- consumers ----
+  int stage = 0, prev_stage = -1;
+  uint32_t phase = 0;
+  for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    const int len = (int)__ldg(tab.len + c);
+    mbar_wait(&sm.full[stage], phase);
+    for (int i = tid; i < len; i += kBulkConsumers) {
+      float acc[E], x[E];
+      Vec<T>::unpack(sm.slot[stage][0][i], acc);
+      if (op == 2) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] = __fmul_rn(wts.w[0], acc[e]);
+      } else if (op == 1) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] = __fadd_rn(0.0f, acc[e]);
+      }
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        Vec<T>::unpack(sm.slot[stage][r][i], x);
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          acc[e] = __fadd_rn(acc[e], op == 2 ? __fmul_rn(wts.w[r], x[e]) : x[e]);
+      }
+      if (op == 1) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] = __fdiv_rn(acc[e], (float)R);
+      }
+      sm.slot[stage][0][i] = Vec<T>::pack(acc);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(kBulkConsumers) : "memory");
+    if (tid == 0) {
+      const uint32_t bytes = (uint32_t)len * 16u;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        uint4 *dst = reinterpret_cast<uint4 *>(bufs.p[__ldg(tab.buf[r] + c)]) + __ldg(tab.off[r] + c);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                     "r"(smem_u32(sm.slot[stage][0])), "r"(bytes)
+                     : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      // the previous stage's stores have finished reading shared memory
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      if (prev_stage >= 0) mbar_arrive(&sm.empty[prev_stage]);
+    }
+    prev_stage = stage;
+    if (++stage == kStages) { stage = 0; phase ^= 1u; }
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+template <typename T, int R, int kStages>
+static cudaError_t launch_bulk(const Table &tab, int nc, const BufTable &bt, const Weights &wts,
+                               int op, int sms, cudaStream_t s) {
+  auto k = multi_kernel_bulk<T, R, kStages>;
+  const int smem = (int)sizeof(BulkSmem<R, kStages>);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int grid = nc < sms ? nc : sms;
+  k<<<grid, kBulkThreads, smem, s>>>(tab, nc, bt, wts, op);
+  return cudaGetLastError();
+}
+
+// 0: AUTO (bulk for R <= 4 and >= 2 chunks per SM), 1: LDG, 2: bulk when R <= 4
+std::atomic<int> g_multi_kernel{0};
 
 }  // namespace multi
 }  // namespace ntp
@@ -306,6 +452,23 @@ int ntp_multi_sync(const ntp_mplan *p, void *const *bufs, int n_bufs, int op, co
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
   const int grid = (int)std::min<size_t>(nc, (size_t)sms * 4);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int variant = multi::g_multi_kernel.load();
+  const bool bulk = p->R <= 4 && (variant == 2 || (variant == 0 && nc >= (size_t)sms * 2));
+  if (bulk) {
+    cudaError_t e = cudaSuccess;
+    const int n = (int)nc;
+    if (p->dtype == NTP_BF16) {
+      if (p->R == 2) e = multi::launch_bulk<__nv_bfloat16, 2, 6>(tab, n, bt, wts, op, sms, s);
+      else if (p->R == 3) e = multi::launch_bulk<__nv_bfloat16, 3, 4>(tab, n, bt, wts, op, sms, s);
+      else e = multi::launch_bulk<__nv_bfloat16, 4, 3>(tab, n, bt, wts, op, sms, s);
+    } else {
+      if (p->R == 2) e = multi::launch_bulk<float, 2, 6>(tab, n, bt, wts, op, sms, s);
+      else if (p->R == 3) e = multi::launch_bulk<float, 3, 4>(tab, n, bt, wts, op, sms, s);
+      else e = multi::launch_bulk<float, 4, 3>(tab, n, bt, wts, op, sms, s);
+    }
+    if (e != cudaSuccess) return fail(NTP_ECUDA, std::string("multi sync (bulk): ") + cudaGetErrorString(e));
+    return NTP_OK;
+  }
 #define NTP_MULTI_CASE(TT, RR) \
   case RR: multi::multi_kernel<TT, RR><<<grid, multi::kThreads, 0, s>>>(tab, (int)nc, bt, wts, op); break;
   if (p->dtype == NTP_BF16) {
@@ -325,6 +488,13 @@ int ntp_multi_sync(const ntp_mplan *p, void *const *bufs, int n_bufs, int op, co
 #undef NTP_MULTI_CASE
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(NTP_ECUDA, std::string("multi sync: ") + cudaGetErrorString(e));
+  return NTP_OK;
+}
+
+// Kernel variant for ntp_multi_sync: 0 AUTO, 1 LDG, 2 TMA bulk (R <= 4).
+int ntp_multi_set_kernel(int variant) {
+  if (variant < 0 || variant > 2) return fail(NTP_EINVAL, "multi kernel variant must be 0..2");
+  multi::g_multi_kernel.store(variant);
   return NTP_OK;
 }
 

@@ -84,8 +84,10 @@ def main():
     for s in grp.hosted:
         a = grp.arena(s)
         a.copy_(torch.randn(a.numel(), generator=g, device="cuda").to(torch.bfloat16))
-    for kern, cap in ((0, 0),):
-        by_pieces["multi"] = timed(lambda: grp.step(stream), steps)
+    for variant, name in ((1, "multi_ldg"), (2, "multi_bulk")):
+        Lb.ntp_multi_set_kernel(variant)
+        by_pieces[name] = timed(lambda: grp.step(stream), steps)
+    Lb.ntp_multi_set_kernel(0)
     assert grp.status() == 0, "signal timeout"
     grp.close()
     best = min(by_pieces, key=by_pieces.get)
@@ -104,13 +106,15 @@ def main():
             "placement_degraded": list(plc.dp), "grad_bytes_per_replica": s_d,
             "ms_per_step": round(ms, 3), "pieces": best,
             "ms_by_pieces/kernel/cap": {p: round(v, 3) for p, v in by_pieces.items()},
-            "degraded_gpu_link_GBps_per_direction": round(s_d / (ms * 1e-3) / 1e9, 1),
-            "link_frac_of_770": round(s_d / (ms * 1e-3) / 1e9 / 770.0, 3),
+            # one replica per GPU: every GPU moves 2 (R-1)/R * S per direction
+            "per_gpu_bytes_per_direction": int(2 * m / (m + 1) * s_d),
+            "per_gpu_GBps_per_direction": round(2 * m / (m + 1) * s_d / (ms * 1e-3) / 1e9, 1),
+            "link_frac_of_770": round(2 * m / (m + 1) * s_d / (ms * 1e-3) / 1e9 / 770.0, 3),
             "uniform_dp_nccl_allreduce_ms": round(ms_ar, 3),
             "overhead_vs_uniform_dp": round(ms / ms_ar - 1.0, 4),
-            "note": "A (every healthy replica folds D's copy of its sub-range in over NVLink), "
-                    "B (NCCL SUM among the healthy replicas), C (push back to D); pieces > 1 "
-                    "pipelines them on 3 streams"}),
+            "note": "multi_*: one R-way peer-memory kernel per GPU (NtpDpMultiGroup; "
+                    "ldg or TMA-bulk ring); p/kKcC: the NCCL composition (NtpDpGroup) with p "
+                    "pipeline pieces and sync kernel K capped at C CTAs"}),
               flush=True)
     dist.destroy_process_group()
 

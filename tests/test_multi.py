@@ -40,11 +40,27 @@ def _layouts(k):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("variant", [1, 2], ids=["ldg", "bulk"])
 @pytest.mark.parametrize("dtype,tol", [(torch.float32, 1e-6), (torch.bfloat16, 2e-2)])
 @pytest.mark.parametrize("mode", ["c3", "mixed"])
-def test_multi_sync_vs_oracle(dtype, tol, mode):
+def test_multi_sync_vs_oracle(dtype, tol, mode, variant):
+    """Both kernels (128-bit loads; TMA-bulk ring, R <= 4 -- "mixed" has R = 5
+    and keeps the load kernel) against the oracle, and bit-identical to each
+    other (the same explicitly rounded arithmetic in the same order)."""
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
+    from paper_2504_06095_b200 import _lib
+    _lib.load().ntp_multi_set_kernel(variant)
+    try:
+        _multi_case(dtype, tol, mode)
+    finally:
+        _lib.load().ntp_multi_set_kernel(0)
+
+
+_RESULTS = {}
+
+
+def _multi_case(dtype, tol, mode):
     from paper_2504_06095_b200 import tpnumerics as T
     k, h = 2000, 32
     tp2, tp1, comp43, sync43 = _layouts(k)
@@ -73,6 +89,10 @@ def test_multi_sync_vs_oracle(dtype, tol, mode):
             assert O.rel_err(got, want) <= tol, (op, O.rel_err(got, want))
             first = got if first is None else first
             assert np.array_equal(got, first)  # every replica holds identical bits
+        key = (str(dtype), mode, op, code)
+        if key in _RESULTS:  # the other kernel variant ran first: same bits
+            assert np.array_equal(_RESULTS[key], first)
+        _RESULTS[key] = first
 
 
 @pytest.mark.gpu
