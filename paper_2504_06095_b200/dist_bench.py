@@ -150,10 +150,17 @@ def run_e2e(args, grp, lay, dtype, eb):
     steps = max(2, min(args.e2e_steps, args.steps))
     ranges = [grp.piece_ranges(i) for i in range(len(grp.pieces))]
 
+    prev = [None]  # per piece: the previous step's D2H of that piece
+
     def one(sync=True):
-        h2d_s.wait_stream(stream)
-        h2d_s.wait_stream(d2h_s)  # the previous step's reads of the host arenas
+        # piece i's H2D waits only for the previous step's D2H of piece i, so
+        # back-to-back steps keep both host-link directions busy
+        if prev[0] is None:
+            h2d_s.wait_stream(stream)
+        done = []
         for i, rg in enumerate(ranges):
+            if prev[0] is not None:
+                h2d_s.wait_event(prev[0][i])
             with torch.cuda.stream(h2d_s):
                 for s, (lo, hi) in rg.items():
                     dev[s][lo:hi].copy_(host[s][lo:hi], non_blocking=True)
@@ -164,6 +171,10 @@ def run_e2e(args, grp, lay, dtype, eb):
             with torch.cuda.stream(d2h_s):
                 for s, (lo, hi) in rg.items():
                     host[s][lo:hi].copy_(dev[s][lo:hi], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(d2h_s)
+            done.append(ev)
+        prev[0] = done
         stream.wait_stream(d2h_s)
 
     one()

@@ -31,6 +31,7 @@ class HostSync:
         self.h2d = torch.cuda.Stream(self.dev)
         self.d2h = torch.cuda.Stream(self.dev)
         self.launches_per_run = 1 if not piece_plans else len(piece_plans)
+        self._d2h_done = None  # per piece: the previous run's D2H of that piece
 
     def run(self, host, w_a: float, w_b: float) -> None:
         """host: pinned CPU tensors, one per arena; synced in place (stream-ordered
@@ -43,8 +44,15 @@ class HostSync:
             for d, h in zip(self.arenas, host):
                 h.copy_(d, non_blocking=True)
             return
-        self.h2d.wait_stream(cur)
-        for plan_i, ranges in self.pieces:
+        # Piece i's H2D waits only for the previous run's D2H of piece i (same
+        # host and device ranges), not for the whole previous run: back-to-back
+        # runs keep both PCIe directions busy across the run boundary.
+        if self._d2h_done is None:
+            self.h2d.wait_stream(cur)
+        done = []
+        for i, (plan_i, ranges) in enumerate(self.pieces):
+            if self._d2h_done is not None:
+                self.h2d.wait_event(self._d2h_done[i])
             with torch.cuda.stream(self.h2d):
                 for a, lo, hi in ranges:
                     self.arenas[a][lo:hi].copy_(host[a][lo:hi], non_blocking=True)
@@ -58,4 +66,8 @@ class HostSync:
             with torch.cuda.stream(self.d2h):
                 for a, lo, hi in ranges:
                     host[a][lo:hi].copy_(self.arenas[a][lo:hi], non_blocking=True)
+            ev3 = torch.cuda.Event()
+            ev3.record(self.d2h)
+            done.append(ev3)
+        self._d2h_done = done
         cur.wait_stream(self.d2h)
