@@ -199,9 +199,9 @@ void ntp_mplan_destroy(ntp_mplan *plan);
  * sum_r w[r]*x_r), written to all R owners; one read and one write per copy. */
 int ntp_multi_sync(const ntp_mplan *plan, void *const *bufs, int n_bufs, int op, const double *w,
                    void *stream);
-/* Kernel for ntp_multi_sync: 0 AUTO (TMA-bulk shared-memory ring for R <= 4
- * and >= 2 chunks per SM, else 128-bit loads), 1 loads, 2 bulk (R <= 4).
- * Both give identical bits. */
+/* Kernel for ntp_multi_sync: 0 AUTO (TMA-bulk shared-memory ring for R <= 4,
+ * >= 2 chunks per SM and at least one peer-mapped copy; else 128-bit loads),
+ * 1 loads, 2 bulk (R <= 4).  Both give identical bits. */
 int ntp_multi_set_kernel(int variant);
 
 /* ------------------------------------------------------------------------

@@ -453,7 +453,18 @@ int ntp_multi_sync(const ntp_mplan *p, void *const *bufs, int n_bufs, int op, co
   const int grid = (int)std::min<size_t>(nc, (size_t)sms * 4);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int variant = multi::g_multi_kernel.load();
-  const bool bulk = p->R <= 4 && (variant == 2 || (variant == 0 && nc >= (size_t)sms * 2));
+  // AUTO: the bulk ring pays off when copies live on peers (NVLink latency);
+  // with every copy in local HBM the 128-bit-load kernel is faster (0.958 vs
+  // 0.922 of HBM on the C3 shape, scripts/multi_bench.py)
+  bool any_peer = false;
+  if (variant == 0)
+    for (int i = 0; i < n_bufs && !any_peer; ++i) {
+      cudaPointerAttributes a{};
+      if (cudaPointerGetAttributes(&a, bufs[i]) == cudaSuccess && a.device != p->device)
+        any_peer = true;
+    }
+  const bool bulk =
+      p->R <= 4 && (variant == 2 || (variant == 0 && any_peer && nc >= (size_t)sms * 2));
   if (bulk) {
     cudaError_t e = cudaSuccess;
     const int n = (int)nc;
