@@ -187,16 +187,36 @@ class DistReconfig:
                     ptrs.append(p)
             self.bufs[name] = ptrs
         self.plans = {}
+        self.split_plans = {}   # dt -> (local-source plan, peer-source plan)
         if units:
             remap = np.full(lay.n_slots(), -1, dtype=np.int64)
             for s, i in self.buf_index.items():
                 remap[s] = i
             batches = self._interleave(units)
+            local_src = self._is_local(remap)
             for dt in set(self.states.values()):
                 plan = Plan(dtype_code(dt))
                 for unit, a_s, a_o, b_s, b_o in batches:
                     plan.add_units(unit, remap[a_s], a_o, remap[b_s], b_o)
                 self.plans[dt] = plan.finalize()
+                parts = []
+                for want_local in (True, False):
+                    part = Plan(dtype_code(dt))
+                    n = 0
+                    for unit, a_s, a_o, b_s, b_o in batches:
+                        sel = local_src[remap[a_s]] == want_local
+                        if sel.any():
+                            part.add_units(unit, remap[a_s][sel], a_o[sel], remap[b_s][sel], b_o[sel])
+                            n += int(sel.sum())
+                    parts.append(part.finalize() if n else None)
+                self.split_plans[dt] = tuple(parts)
+        # "interleaved" (default): one kernel per state tensor, local copies and
+        # peer pulls interleaved in its chunk order; "split": two kernels on two
+        # streams, the peer one capped to `peer_ctas` SMs -- measured no faster
+        # (profiles/r01_dist_reconfig.json)
+        self.launch_mode = "interleaved"
+        self.peer_ctas = 40
+        self._side = None
 
     def _interleave(self, units):
         """Order the pulled units so local copies (HBM-bound) and peer reads
@@ -224,9 +244,18 @@ class DistReconfig:
             out.append((int(u[lo]), a_s[lo:hi], a_o[lo:hi], b_s[lo:hi], b_o[lo:hi]))
         return out
 
+    def _is_local(self, remap):
+        """bool per dense buffer index: the buffer lives on this process."""
+        order = sorted(self.buf_index, key=self.buf_index.get)
+        return np.asarray([self.proc[s] == self.rank for s in order], dtype=bool)
+
     def upload(self) -> "DistReconfig":
         for p in self.plans.values():
             p.upload(self.device)
+        for parts in self.split_plans.values():
+            for p in parts:
+                if p is not None:
+                    p.upload(self.device)
         return self
 
     def arena(self, slot: int, name: str) -> torch.Tensor:
@@ -244,9 +273,34 @@ class DistReconfig:
 
     def launch(self, stream=None) -> None:
         """The copies alone (no barriers): the caller orders them."""
-        for name, dt in self.states.items():
-            if dt in self.plans:
-                self.plans[dt].reshard(self.bufs[name], stream)
+        if self.launch_mode != "split":
+            for name, dt in self.states.items():
+                if dt in self.plans:
+                    self.plans[dt].reshard(self.bufs[name], stream)
+            return
+        from . import _lib
+        L = _lib.load()
+        main = torch.cuda.current_stream(self.device) if stream is None else stream
+        if self._side is None:
+            self._side = torch.cuda.Stream(self.device)
+        side = self._side
+        side.wait_stream(main)
+        sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+        old_cap = int(L.ntp_get_option(1))
+        try:
+            for name, dt in self.states.items():
+                if dt not in self.split_plans:
+                    continue
+                local, peer = self.split_plans[dt]
+                if peer is not None:
+                    L.ntp_set_option(1, self.peer_ctas)
+                    peer.reshard(self.bufs[name], side)
+                if local is not None:
+                    L.ntp_set_option(1, max(1, sms - self.peer_ctas) if peer is not None else 0)
+                    local.reshard(self.bufs[name], main)
+        finally:
+            L.ntp_set_option(1, old_cap)
+        main.wait_stream(side)
 
     def bytes_pulled(self) -> dict:
         """Algorithmic bytes this process moves, split into local and over the link."""
