@@ -253,7 +253,11 @@ int ntp_gemm_bf16_ex(const void *A, int64_t lda, int a_mn, const void *B, int64_
  * mode 2 (push, TMA): as mode 1, but each 32-row output box whose rows are
  * consecutive rows of one partner copy is sent as one TMA tensor store over
  * NVLink from the same shared-memory staging as the local store; other boxes
- * (run boundaries, ragged tails) fall back to row stores. */
+ * (run boundaries, ragged tails) fall back to row stores.
+ * mode 3 (red, TMA): as mode 0 (zeroed arenas), but every box is added with
+ * TMA bulk tensor reductions (cp.reduce.async.bulk.tensor .add) into the
+ * local copy and the partner copy; row red.adds where a box's rows are not
+ * consecutive in the partner's layout. */
 int ntp_gemm_bf16_red(const void *A, int64_t lda, int a_mn, const void *B, int64_t ldb, int b_mn,
                       void *C, int64_t ldc, int c_f32, int64_t M, int64_t N, int64_t K,
                       float alpha, const int32_t *red_buf, const int32_t *red_row,

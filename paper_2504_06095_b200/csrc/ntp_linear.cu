@@ -170,6 +170,10 @@ struct Params {
   // of one peer copy goes there as one TMA tensor store (peer_maps[pb]) from the
   // same smem staging as the local store; other boxes fall back to row stores
   int push_tma;
+  // EPI_RED with tma_red = 1: the box is added into the local copy and the
+  // partner's copy with TMA bulk tensor reductions (cp.reduce.async.bulk.tensor
+  // .add) from the same smem staging -- no per-thread remote atomics
+  int tma_red;
   // programmatic dependent launch: 0 off; 1 = wait for the previous kernel in
   // the stream before touching global memory (prologue overlaps its tail);
   // 2 = this GEMM's inputs and outputs are independent of the previous kernel
@@ -286,6 +290,14 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, const void 
                    reinterpret_cast<uint64_t>(map)),
                "r"(c0), "r"(c1), "r"(smem_u32(smem_src))
                : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap *map, const void *smem_src,
+                                                  int c0, int c1) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(smem_u32(smem_src))
+      : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -487,7 +499,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         if (col0 >= p.N || row0 >= p.M) return;  // warp-uniform: nothing of this box is stored
 #pragma unroll
         for (int j = 0; j < 32; ++j) f[j] *= p.alpha;
-        if (p.epi == EPI_RED || (p.epi == EPI_PUSH && !p.push_tma)) {
+        if ((p.epi == EPI_RED && !p.tma_red) || (p.epi == EPI_PUSH && !p.push_tma)) {
           // fused sync: this replica's weighted contribution goes into its own copy
           // and, over NVLink, into the partner replica's copy (EPI_RED: red.add
           // into zeroed arenas) or the partner's staging arena (EPI_PUSH: plain
@@ -579,7 +591,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         // -- one TMA store over NVLink when its 32 rows are consecutive rows of
         // one peer copy, else row stores from registers (run boundaries, ragged M)
         int peer_box = -1, peer_row0 = 0;
-        if (p.epi == EPI_PUSH) {
+        const bool reduce = p.epi == EPI_RED;  // only reached with tma_red
+        if (p.epi == EPI_PUSH || reduce) {
           const int pb = row < p.M ? p.red_buf[row] : -1;
           const int pr = row < p.M ? p.red_row[row] : 0;
           const int pb0 = __shfl_sync(0xffffffffu, pb, 0), pr0 = __shfl_sync(0xffffffffu, pr, 0);
@@ -588,13 +601,20 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             peer_row0 = pr0;
           } else if (pb >= 0 && col0 + 32 <= p.N) {
             const int ce = p.c_f32 ? 4 : 2;
-            store_row32(p.red_base[pb] + ((long long)pr * p.red_ld + col0) * ce, f, p.c_f32);
+            char *dst = p.red_base[pb] + ((long long)pr * p.red_ld + col0) * ce;
+            if (reduce) red_row32(dst, f, p.c_f32);
+            else store_row32(dst, f, p.c_f32);
           }
         }
         if (lane == 0) {
-          if (p.c_tma) tma_store_2d(&map_c, stage, col0, row0);  // TMA clips rows >= M, cols >= N
-          if (p.epi == EPI_GELU && p.h_tma) tma_store_2d(&map_h, stage + 2048, col0, row0);
-          if (peer_box >= 0) tma_store_2d(&peer_maps.m[peer_box], stage, col0, peer_row0);
+          if (reduce) {
+            tma_reduce_add_2d(&map_c, stage, col0, row0);
+            if (peer_box >= 0) tma_reduce_add_2d(&peer_maps.m[peer_box], stage, col0, peer_row0);
+          } else {
+            if (p.c_tma) tma_store_2d(&map_c, stage, col0, row0);  // TMA clips rows >= M, cols >= N
+            if (p.epi == EPI_GELU && p.h_tma) tma_store_2d(&map_h, stage + 2048, col0, row0);
+            if (peer_box >= 0) tma_store_2d(&peer_maps.m[peer_box], stage, col0, peer_row0);
+          }
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
         if (!p.c_tma) box_store(stage, p.C, p.ldc, p.c_f32 ? 4 : 2, row0, col0, p.M, p.N, lane);
@@ -888,17 +908,20 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
   p.ldh = ldh;
   PeerMaps pm;
   memset(&pm, 0, sizeof pm);
-  if (p.epi == EPI_PUSH && p.push_tma) {
+  const bool c_aligned = !((reinterpret_cast<uintptr_t>(C) & 15u) || ((ldc * ce) & 15));
+  if (p.epi == EPI_RED && p.tma_red && !c_aligned) p.tma_red = 0;  // per-thread red.add path
+  if ((p.epi == EPI_PUSH && p.push_tma) || (p.epi == EPI_RED && p.tma_red)) {
     // rows: any row a box is checked to own (red_row) -- the extent only bounds the map
-    for (int i = 0; i < kMaxPeers && p.push_tma; ++i)
+    bool ok = true;
+    for (int i = 0; i < kMaxPeers && ok; ++i)
       if (p.red_base[i] &&
           make_map(&pm.m[i], p.red_base[i],
                    p.c_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : BF, ce, p.N, 1ll << 24, p.red_ld,
                    32, 32, NOSW))
-        p.push_tma = 0;  // unaligned peer copy: row stores only
+        ok = false;
+    if (!ok) p.push_tma = p.tma_red = 0;  // unaligned peer copy: per-row stores / red.add
   }
-  p.c_tma = p.epi != EPI_RED && (p.epi != EPI_PUSH || p.push_tma) &&
-            !((reinterpret_cast<uintptr_t>(C) & 15u) || ((ldc * ce) & 15));
+  p.c_tma = (p.epi != EPI_RED || p.tma_red) && (p.epi != EPI_PUSH || p.push_tma) && c_aligned;
   p.h_tma = p.epi == EPI_GELU && !((reinterpret_cast<uintptr_t>(H) & 15u) || ((ldh * 2) & 15));
   memset(&mc, 0, sizeof mc);
   memset(&mh, 0, sizeof mh);
@@ -1027,8 +1050,9 @@ extern "C" int ntp_gemm_bf16_red(const void *A, int64_t lda, int a_mn, const voi
                                  const int32_t *red_buf, const int32_t *red_row,
                                  void *const *red_base, int n_red, int64_t red_ld, int mode,
                                  void *stream) {
-  if (mode < 0 || mode > 2)
-    return fail(NTP_EINVAL, "fused mode must be 0 (red), 1 (push) or 2 (push, TMA boxes)");
+  if (mode < 0 || mode > 3)
+    return fail(NTP_EINVAL,
+                "fused mode must be 0 (red), 1 (push), 2 (push, TMA boxes) or 3 (red, TMA boxes)");
   if (M <= 0 || N <= 0 || K <= 0) return fail(NTP_EINVAL, "GEMM extents must be positive");
   if (N % 32) return fail(NTP_EINVAL, "fused sync GEMM needs N % 32 == 0");
   if (n_red < 0 || n_red > gemm::kMaxPeers) return fail(NTP_EINVAL, "at most 8 peer copies");
@@ -1037,7 +1061,8 @@ extern "C" int ntp_gemm_bf16_red(const void *A, int64_t lda, int a_mn, const voi
   if ((reinterpret_cast<uintptr_t>(C) & 15u) || ((ldc * ce) & 15) || ((red_ld * ce) & 15))
     return fail(NTP_EINVAL, "fused sync GEMM needs 16-byte aligned rows");
   gemm::Params p{(int)M, (int)N, (int)K, a_mn ? 1 : 0, b_mn ? 1 : 0, c_f32 ? 1 : 0,
-                 mode ? gemm::EPI_PUSH : gemm::EPI_RED, nullptr, 0, alpha, 0, 0, nullptr,
+                 (mode == 1 || mode == 2) ? gemm::EPI_PUSH : gemm::EPI_RED, nullptr, 0, alpha,
+                 0, 0, nullptr,
                  nullptr, 0, 0, 0, 0};
   p.red_buf = red_buf;
   p.red_row = red_row;
@@ -1048,6 +1073,7 @@ extern "C" int ntp_gemm_bf16_red(const void *A, int64_t lda, int a_mn, const voi
       return fail(NTP_EINVAL, "peer copies must be 16-byte aligned");
   p.red_ld = red_ld;
   p.push_tma = mode == 2;
+  p.tma_red = mode == 3;
   p.pdl = gemm::g_pdl.load();
   return gemm::dispatch(A, lda, a_mn, B, ldb, b_mn, C, ldc, nullptr, 0, p,
                         static_cast<cudaStream_t>(stream));

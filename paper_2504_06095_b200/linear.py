@@ -88,8 +88,10 @@ def mm(A: torch.Tensor, Bt: torch.Tensor, out: torch.Tensor, *, epilogue: str = 
 
 # "red": red.add into zeroed arenas; "push": row stores into the partner's
 # staging arena; "push_tma": the same, but 32-row boxes whose rows are
-# consecutive in the partner's layout go as one TMA tensor store over NVLink
-FUSED_MODES = {"red": 0, "push": 1, "push_tma": 2}
+# consecutive in the partner's layout go as one TMA tensor store over NVLink;
+# "red_tma": zeroed arenas like "red", every box added with TMA bulk tensor
+# reductions (cp.reduce.async.bulk.tensor .add) -- no staging, no local tail
+FUSED_MODES = {"red": 0, "push": 1, "push_tma": 2, "red_tma": 3}
 
 
 def mm_red(A: torch.Tensor, Bt: torch.Tensor, out: torch.Tensor, alpha: float,

@@ -49,7 +49,7 @@ def main():
     lay = pair_layout(ModelShape("fused", h, k, 0, 1), n1, n2)
     plc = Placement.default(world, n1, n2)
     grp = NtpSyncGroup(lay, plc, torch.float32, local).upload()
-    stg = NtpSyncGroup(lay, plc, torch.float32, local).upload() if mode != "red" else None
+    stg = NtpSyncGroup(lay, plc, torch.float32, local).upload() if mode in ("push", "push_tma") else None
     _, unit, hc, rc, _, _ = lay.segs[0]
     rng = np.random.default_rng(5)  # identical on every rank
     bf = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(torch.bfloat16)  # noqa: E731
@@ -65,12 +65,12 @@ def main():
         sh = MlpShard(A, B, cols)
         sh.forward(bf(X).cuda(), torch.empty((X.shape[0], h), device="cuda"))
         slots = [n1 + j for j in range(n2)] if healthy else list(range(n1))
-        ptrs = (grp if mode == "red" else stg).open_slots(slots)
+        ptrs = (grp if mode in ("red", "red_tma") else stg).open_slots(slots)
         rb, rr = partner_row_map(cols, rc if healthy else hc, "cuda")
         work.append((sh, bf(X).cuda(), bf(G).cuda(), grp.arena(s).view(len(cols), 2, h),
                      w_h if healthy else w_r, rb, rr, ptrs, s))
     e = 1
-    if mode == "red":
+    if mode in ("red", "red_tma"):
         for s in grp.hosted:
             grp.arena(s).zero_()
     grp.signal("post_ready", e)
@@ -79,7 +79,7 @@ def main():
         sh.backward_synced(X, G, grads, alpha, rb, rr, [_P(p) for p in ptrs], mode=mode)
     grp.signal("post_done", e)
     grp.signal("wait_done", e)
-    if mode != "red":
+    if stg is not None:
         for sh, X, G, grads, alpha, rb, rr, ptrs, s in work:
             finish_push(grp.arena(s), stg.arena(s))
     torch.cuda.synchronize()

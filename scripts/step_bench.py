@@ -133,24 +133,24 @@ class Config:
         for li in range(self.L):
             gr = self.groups[li]
             gr.epoch += 1
-            if mode == "red":
+            if mode in ("red", "red_tma"):
                 for s in gr.hosted:
                     gr.arena(s).zero_()
             gr.signal("post_ready", gr.epoch, main)
             gr.signal("wait_ready", gr.epoch, main)
         for li in reversed(range(self.L)):
             for sh, X, G, grads, alpha, rb, rr, ptrs, sptrs, st in self.fused[li]:
-                tgt = ptrs if mode == "red" else sptrs
+                tgt = ptrs if mode in ("red", "red_tma") else sptrs
                 sh.backward_synced(X, G, grads, alpha, rb, rr, [_P(p) for p in tgt], main, mode)
             self.groups[li].signal("post_done", self.groups[li].epoch, main)
-            if mode != "red":
+            if mode in ("push", "push_tma"):
                 # the layer's local tail (arena += partner's staging) runs on the
                 # side stream under the next layers' GEMMs
                 side.wait_stream(main)
                 self.groups[li].signal("wait_done", self.groups[li].epoch, side)
                 for sh, X, G, grads, alpha, rb, rr, ptrs, sptrs, st in self.fused[li]:
                     finish_push(grads, st, side)
-        if mode == "red":
+        if mode in ("red", "red_tma"):
             for li in range(self.L):
                 self.groups[li].signal("wait_done", self.groups[li].epoch, main)
         else:
@@ -242,6 +242,7 @@ def modes(Lb, sms):
         "fused_red": (opts(), lambda c: c.fused_backward("red")),
         "fused_push": (opts(), lambda c: c.fused_backward("push")),
         "fused_push_tma": (opts(), lambda c: c.fused_backward("push_tma")),
+        "fused_red_tma": (opts(), lambda c: c.fused_backward("red_tma")),
         "fused_push_tma_ldg_cap74": (opts(1, 74), lambda c: c.fused_backward("push_tma")),
     }
 

@@ -72,7 +72,7 @@ def test_eight_gpus_c3():
     _run_script(8, "dp_check.py", 3, 2, 1, "bf16", 2)
 
 
-@pytest.mark.parametrize("mode", ["red", "push", "push_tma"])
+@pytest.mark.parametrize("mode", ["red", "push", "push_tma", "red_tma"])
 @pytest.mark.parametrize("n,n1,n2", [(2, 2, 1), (4, 2, 1), (2, 4, 3)])
 def test_fused_wgrad_sync_multi_gpu(n, n1, n2, mode):
     """tcgen05 wgrad epilogues send this replica's weighted gradient to the

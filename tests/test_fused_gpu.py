@@ -20,8 +20,11 @@ def mods():
     return linear, tpnumerics
 
 
+@pytest.mark.parametrize("mode", ["red", "red_tma"])
 @pytest.mark.parametrize("gdtype,tol", [(torch.float32, 1e-5), (torch.bfloat16, 1e-2)])
-def test_fused_backward_sync_matches_unfused(mods, gdtype, tol):
+def test_fused_backward_sync_matches_unfused(mods, gdtype, tol, mode):
+    """mode "red": per-thread red.add; "red_tma": TMA bulk tensor reductions of
+    whole 32 x 32 boxes into both arenas (row red.adds at run boundaries)."""
     Lin, T = mods
     from paper_2504_06095_b200.shardmap import build_shard_map
     h, k, tok_h, tok_r = 128, 1000, 256, 192
@@ -54,10 +57,10 @@ def test_fused_backward_sync_matches_unfused(mods, gdtype, tol):
     fr = T.MlpReplica(layer, rc, dtype=gdtype)
     for sh, cols, g in zip(sh_h, hc, fh.grads):
         rb, rr = Lin.partner_row_map(cols, rc, "cuda")
-        sh.backward_synced(bf(Xh).cuda(), bf(Gh).cuda(), g, w_h, rb, rr, fr.grads)
+        sh.backward_synced(bf(Xh).cuda(), bf(Gh).cuda(), g, w_h, rb, rr, fr.grads, mode=mode)
     for sh, cols, g in zip(sh_r, rc, fr.grads):
         rb, rr = Lin.partner_row_map(cols, hc, "cuda")
-        sh.backward_synced(bf(Xr).cuda(), bf(Gr).cuda(), g, w_r, rb, rr, fh.grads)
+        sh.backward_synced(bf(Xr).cuda(), bf(Gr).cuda(), g, w_r, rb, rr, fh.grads, mode=mode)
     fh._has_grads = fr._has_grads = True
     torch.cuda.synchronize()
     # both replicas identical bit for bit
