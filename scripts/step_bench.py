@@ -130,15 +130,32 @@ class Config:
 
     def fused_backward(self, mode="red"):
         main, side = self.main, self.side
-        for li in range(self.L):
-            gr = self.groups[li]
-            gr.epoch += 1
-            if mode in ("red", "red_tma"):
-                for s in gr.hosted:
-                    gr.arena(s).zero_()
-            gr.signal("post_ready", gr.epoch, main)
-            gr.signal("wait_ready", gr.epoch, main)
+        red = mode in ("red", "red_tma")
+        if red:
+            # zero each layer's arena on the side stream (in backward order) and
+            # tell the partners; a layer's GEMMs wait for both ends' zeroing
+            side.wait_stream(main)
+            zeroed = {}
+            for li in reversed(range(self.L)):
+                gr = self.groups[li]
+                gr.epoch += 1
+                with torch.cuda.stream(side):
+                    for s in gr.hosted:
+                        gr.arena(s).zero_()
+                gr.signal("post_ready", gr.epoch, side)
+                ev = torch.cuda.Event()
+                ev.record(side)
+                zeroed[li] = ev
+        else:
+            for li in range(self.L):
+                gr = self.groups[li]
+                gr.epoch += 1
+                gr.signal("post_ready", gr.epoch, main)
+                gr.signal("wait_ready", gr.epoch, main)
         for li in reversed(range(self.L)):
+            if red:
+                main.wait_event(zeroed[li])
+                self.groups[li].signal("wait_ready", self.groups[li].epoch, main)
             for sh, X, G, grads, alpha, rb, rr, ptrs, sptrs, st in self.fused[li]:
                 tgt = ptrs if mode in ("red", "red_tma") else sptrs
                 sh.backward_synced(X, G, grads, alpha, rb, rr, [_P(p) for p in tgt], main, mode)
