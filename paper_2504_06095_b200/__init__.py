@@ -10,6 +10,7 @@ Public API mirrors the reference package ``ntpsim``:
 * ``dist_dp``    -- DP > 2 with one degraded replica (NCCL among the healthy ones)
 * ``dist_reconfig`` -- the failure reconfiguration across processes (peer pulls)
 * ``linear``     -- tcgen05 uneven-shard MLP linears writing the unit-major arenas
+* ``step``       -- the degraded-replica backward with every layer's sync overlapped
 
 All device work runs in libntp_b200.so (csrc/, sm_100a); there is no CPU
 fallback.

@@ -86,3 +86,10 @@ def test_failure_reconfig_multi_gpu(n, n1, dead):
     """dist_reconfig: H -> comp layout, D's survivors -> TP-(n1-1), the dead
     rank's units pulled from H over NVLink; bit-exact for bf16 and fp32 state."""
     _run_script(n, "reconfig_check.py", "check", n1, dead)
+
+
+@pytest.mark.parametrize("n,n1,n2", [(2, 2, 1), (4, 2, 1)])
+def test_overlapped_backward_step(n, n1, n2):
+    """paper_2504_06095_b200.step.OverlappedBackward: the overlapped product
+    step gives the same bits as GEMMs-then-syncs."""
+    _run_script(n, "step_check.py", n1, n2, 3)
