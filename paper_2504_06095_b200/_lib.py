@@ -119,8 +119,10 @@ def load():
         if _lib is not None:
             return _lib
         path = _build.LIB
+        if os.environ.get("NTP_LIB_AB"):  # A/B experiments only: another build of the same ABI
+            path = os.environ["NTP_LIB_AB"]
         try:
-            if _build._stale() and os.path.exists(_build.NVCC):
+            if path == _build.LIB and _build._stale() and os.path.exists(_build.NVCC):
                 _build.build()
         except Exception as e:  # pragma: no cover - surfaced below
             if not os.path.exists(path):

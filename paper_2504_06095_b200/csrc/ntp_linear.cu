@@ -77,6 +77,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     if (t - t0 > 4000000000ull) asm volatile("trap;");
   }
 }
+// Long waits (the epilogue waiting a whole tile for its accumulator): poll
+// with a short sleep so the spinning warps leave issue slots to the producer
+// and MMA warps that share their SM sub-partitions.
+__device__ __forceinline__ void mbar_wait_sleepy(uint64_t *bar, uint32_t parity) {
+  if (mbar_try(bar, parity)) return;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (!mbar_try(bar, parity)) {
+    __nanosleep(64);
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 4000000000ull) asm volatile("trap;");
+  }
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void tma_load_2d(void *smem_dst, const CUtensorMap *map, int c0, int c1,
                                             uint64_t *bar) {
   asm volatile(
@@ -179,7 +200,22 @@ struct Params {
   // 2 = this GEMM's inputs and outputs are independent of the previous kernel
   // (runs under its tail), but the grid does not complete before it does
   int pdl;
+  // tile order: tiles are walked in groups of `raster` M-tile rows (M fastest
+  // inside a group); 0 = one group of all M rows
+  int raster;
+  int epi_sleep;  // 1: the epilogue polls its accumulator barrier with a sleep
+  int debug;      // experiments: 1 = no operand loads, 2 = no epilogue output,
+                  // 4 = MMA skips the full-stage waits, 8 = no stage commits (no producer)
 };
+
+// tile t -> (M-tile, N-tile) under the grouped raster order
+__device__ __forceinline__ void tile_coords(int t, const Params &p, int &tm, int &tn) {
+  const int G = (p.raster > 0 && p.raster < p.num_m) ? p.raster : p.num_m;
+  const int span = G * p.num_n, g = t / span, w = t - g * span;
+  const int gsz = min(G, p.num_m - g * G);
+  tm = g * G + w % gsz;
+  tn = w / gsz;
+}
 
 // Tensor maps over the peer copies (EPI_PUSH, push_tma): boxes of 32 x 32 at
 // the GEMM output's element type, row pitch red_ld.
@@ -251,21 +287,30 @@ __device__ __forceinline__ void red_row32(void *dst, const float *f, int c_f32) 
   }
 }
 
+// Staged 32 x 32 output boxes are swizzled like the TMA maps that store them
+// (fp32: 128-byte rows, SWIZZLE_128B; bf16: 64-byte rows, SWIZZLE_64B): the
+// 16-byte chunk c of row r sits at chunk c ^ swz(r), so the 32 lanes of a warp
+// (one row each) write conflict-free instead of all hitting the same banks.
+__device__ __forceinline__ int stage_swz(int r, int esize) {
+  return esize == 4 ? (r & 7) : ((r >> 1) & 3);
+}
+
 // Copy a staged 32 x 32 box to global with row/column masking (pitches a TMA
 // map cannot describe).  esize = 2 (bf16) or 4 (fp32).
 __device__ __forceinline__ void box_store(const unsigned char *stage, void *g, long long ld,
                                           int esize, int row0, int col0, int M, int N, int lane) {
   const int col = col0 + lane;
   if (col >= N) return;
+  const int b = lane * esize, rp = 32 * esize;
   for (int r = 0; r < 32; ++r) {
     const int row = row0 + r;
     if (row >= M) break;
+    const unsigned char *src = stage + r * rp + ((((b >> 4) ^ stage_swz(r, esize)) << 4) | (b & 15));
     if (esize == 4)
-      reinterpret_cast<float *>(g)[(long long)row * ld + col] =
-          reinterpret_cast<const float *>(stage)[r * 32 + lane];
+      reinterpret_cast<float *>(g)[(long long)row * ld + col] = *reinterpret_cast<const float *>(src);
     else
       reinterpret_cast<__nv_bfloat16 *>(g)[(long long)row * ld + col] =
-          reinterpret_cast<const __nv_bfloat16 *>(stage)[r * 32 + lane];
+          *reinterpret_cast<const __nv_bfloat16 *>(src);
   }
 }
 
@@ -276,7 +321,7 @@ template <int BN, int kPair, int kStg>
 struct Smem {
   alignas(1024) __nv_bfloat16 a[kStg][BM * BK];
   alignas(1024) __nv_bfloat16 b[kStg][(BN / kPair) * BK];
-  alignas(128) unsigned char out[4][2][kStageBytes];  // double-buffered per epilogue warp
+  alignas(1024) unsigned char out[4][2][kStageBytes];  // double-buffered per epilogue warp (swizzled)
   uint64_t full[kStg];
   uint64_t empty[kStg];
   uint64_t tmem_full[2];
@@ -414,11 +459,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       // ---- TMA producer (both CTAs of a pair) ----
       const uint32_t cta_bytes = (BM + BNC) * BK * 2;
       int it = 0, plocal = 0;
-      for (int item = unit_id; item < num_items; item += num_units, ++plocal) {
+      for (int item = unit_id; item < num_items && !(p.debug & 8); item += num_units, ++plocal) {
         const Work w = decode_work(item, p, nk);
         const int t = w.t;
-        const int m0 = (t % p.num_m) * TM + (int)rank * BM;
-        const int n0 = (t / p.num_m) * BN + (int)rank * BNC;
+        int tm, tn;
+        tile_coords(t, p, tm, tn);
+        const int m0 = tm * TM + (int)rank * BM;
+        const int n0 = tn * BN + (int)rank * BNC;
         unsigned long long *trp =
             p.trace && plocal < kTraceItems ? p.trace + ((size_t)blockIdx.x * kTraceItems + plocal) * 8 : nullptr;
         for (int kb = w.kb_lo; kb < w.kb_hi; ++kb, ++it) {
@@ -426,6 +473,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
           mbar_wait(&sm.empty[s], ((it / kStg) & 1) ^ 1);
           if (trp && kb == w.kb_lo) trp[4] = gtime();
           if (trp && kb == w.kb_hi - 1) trp[5] = gtime();
+          if (p.debug & 1) {  // debug: no operand loads (MMA ceiling on stale smem)
+            if (leader) mbar_arrive(&sm.full[s]);
+            continue;
+          }
           if (leader) mbar_expect_tx(&sm.full[s], cta_bytes * kPair);
           const int k0 = kb * BK;
           auto load = [&](void *dst, const CUtensorMap *m, int c0, int c1) {
@@ -448,14 +499,20 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
+    if (leader) {
       // ---- MMA issuer (the leader CTA of a pair) ----
+      // The whole warp walks the schedule (every value below is warp-uniform,
+      // so the descriptors live in uniform registers) and one elected lane
+      // issues the MMAs and commits -- no per-MMA uniform-register waterfall.
       const uint32_t idesc = instr_desc(TM, BN, p.a_mn, p.b_mn);
       // K-major: rows of 128 B, 8-row atoms 1024 B apart (SBO); K advance +32 B per k16.
       // MN-major: 64-element MN blocks of BK rows (LBO = BK*128 B), 8-row K groups
       // 1024 B apart (SBO); K advance +2048 B per k16.
       const uint32_t a_lbo = p.a_mn ? BK * 128 : 16, b_lbo = p.b_mn ? BK * 128 : 16;
       const uint32_t k_step_a = p.a_mn ? 2048u : 32u, k_step_b = p.b_mn ? 2048u : 32u;
+      const uint64_t ad0 = smem_desc(smem_u32(sm.a[0]), a_lbo, 1024);
+      const uint64_t bd0 = smem_desc(smem_u32(sm.b[0]), b_lbo, 1024);
+      constexpr uint32_t a_stage16 = (BM * BK * 2) >> 4, b_stage16 = (BNC * BK * 2) >> 4;
       int it = 0, local = 0;
       for (int item = unit_id; item < num_items; item += num_units, ++local) {
         const Work w = decode_work(item, p, nk);
@@ -464,26 +521,34 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(acc * BN);
         unsigned long long *trp =
-            p.trace && local < kTraceItems ? p.trace + ((size_t)blockIdx.x * kTraceItems + local) * 8 : nullptr;
+            p.trace && lane == 0 && local < kTraceItems ? p.trace + ((size_t)blockIdx.x * kTraceItems + local) * 8 : nullptr;
         for (int kb = w.kb_lo; kb < w.kb_hi; ++kb, ++it) {
           const int s = it % kStg;
-          mbar_wait(&sm.full[s], (it / kStg) & 1);
+          if (!(p.debug & 4)) mbar_wait(&sm.full[s], (it / kStg) & 1);
           if (trp && kb == w.kb_lo) trp[6] = gtime();
           if (trp && kb == w.kb_hi - 1) trp[7] = gtime();
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(sm.a[s]), b_addr = smem_u32(sm.b[s]);
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t ad = smem_desc(a_addr + kk * k_step_a, a_lbo, 1024);
-            const uint64_t bd = smem_desc(b_addr + kk * k_step_b, b_lbo, 1024);
-            const uint32_t accum = (kb > w.kb_lo || kk) ? 1u : 0u;
-            if constexpr (kPair == 2) tc_mma2(d, ad, bd, idesc, accum);
-            else tc_mma(d, ad, bd, idesc, accum);
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              // descriptors advance in 16-byte units in their low field
+              const uint64_t ad = ad0 + (uint64_t)(s * a_stage16 + ((kk * k_step_a) >> 4));
+              const uint64_t bd = bd0 + (uint64_t)(s * b_stage16 + ((kk * k_step_b) >> 4));
+              const uint32_t accum = (kb > w.kb_lo || kk) ? 1u : 0u;
+              if constexpr (kPair == 2) tc_mma2(d, ad, bd, idesc, accum);
+              else tc_mma(d, ad, bd, idesc, accum);
+            }
+            // frees the stage (in both CTAs) once these MMAs have read it
+            if (!(p.debug & 8)) {
+              if constexpr (kPair == 2) tc_commit2(&sm.empty[s], 0x3); else tc_commit(&sm.empty[s]);
+            }
           }
-          // frees the stage (in both CTAs) once these MMAs have read it
-          if constexpr (kPair == 2) tc_commit2(&sm.empty[s], 0x3); else tc_commit(&sm.empty[s]);
+          __syncwarp();
         }
-        if constexpr (kPair == 2) tc_commit2(&sm.tmem_full[acc], 0x3); else tc_commit(&sm.tmem_full[acc]);
+        if (elect_one()) {
+          if constexpr (kPair == 2) tc_commit2(&sm.tmem_full[acc], 0x3); else tc_commit(&sm.tmem_full[acc]);
+        }
+        __syncwarp();
       }
     }
   } else {
@@ -531,6 +596,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
           // H = bf16(acc) (kept for the backward), Y = GeLU(H)
           uint4 *hs = reinterpret_cast<uint4 *>(stage + 2048 + lane * 64);
           uint4 *ys = reinterpret_cast<uint4 *>(stage + lane * 64);
+          const int sw = stage_swz(lane, 2);
 #pragma unroll
           for (int j = 0; j < 32; j += 8) {
             uint32_t hw[4], yw[4];
@@ -542,8 +608,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
               hw[e] = *reinterpret_cast<uint32_t *>(&hh);
               yw[e] = *reinterpret_cast<uint32_t *>(&yy);
             }
-            hs[j / 8] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-            ys[j / 8] = make_uint4(yw[0], yw[1], yw[2], yw[3]);
+            hs[(j / 8) ^ sw] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            ys[(j / 8) ^ sw] = make_uint4(yw[0], yw[1], yw[2], yw[3]);
           }
         } else {
           if (p.epi == EPI_DGELU && row < p.M) {
@@ -569,10 +635,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
           }
           if (p.c_f32) {
             float4 *cs = reinterpret_cast<float4 *>(stage + lane * 128);
+            const int sw = stage_swz(lane, 4);
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) cs[j / 4] = make_float4(f[j], f[j + 1], f[j + 2], f[j + 3]);
+            for (int j = 0; j < 32; j += 4)
+              cs[(j / 4) ^ sw] = make_float4(f[j], f[j + 1], f[j + 2], f[j + 3]);
           } else {
             uint4 *cs = reinterpret_cast<uint4 *>(stage + lane * 64);
+            const int sw = stage_swz(lane, 2);
 #pragma unroll
             for (int j = 0; j < 32; j += 8) {
               uint32_t w[4];
@@ -581,7 +650,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                 __nv_bfloat162 tt = __floats2bfloat162_rn(f[j + 2 * e], f[j + 2 * e + 1]);
                 w[e] = *reinterpret_cast<uint32_t *>(&tt);
               }
-              cs[j / 8] = make_uint4(w[0], w[1], w[2], w[3]);
+              cs[(j / 8) ^ sw] = make_uint4(w[0], w[1], w[2], w[3]);
             }
           }
         }
@@ -626,7 +695,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       const Work w = decode_work(item, p, nk);
       const int t = w.t;
       const int acc = local & 1;
-      const int m0 = (t % p.num_m) * TM + (int)rank * BM, n0 = (t / p.num_m) * BN;
+      int tm, tn;
+      tile_coords(t, p, tm, tn);
+      const int m0 = tm * TM + (int)rank * BM, n0 = tn * BN;
       const int row0 = m0 + q * 32;
       // split-K piece: this warp's 32 x BN partial lives in ws, float4 column
       // groups outermost so each warp access is 512 contiguous bytes
@@ -634,7 +705,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
           ? reinterpret_cast<float4 *>(
                 p.ws + ((((size_t)w.tail * p.split + w.piece) * kPair + rank) * 4 + q) * 32 * BN)
           : nullptr;
-      mbar_wait(&sm.tmem_full[acc], (local >> 1) & 1);
+      if (p.epi_sleep) mbar_wait_sleepy(&sm.tmem_full[acc], (local >> 1) & 1);
+      else mbar_wait(&sm.tmem_full[acc], (local >> 1) & 1);
       const bool tr = p.trace && q == 0 && lane == 0 && local < kTraceItems;
       unsigned long long *trp = tr ? p.trace + ((size_t)blockIdx.x * kTraceItems + local) * 8 : nullptr;
       if (tr) { trp[0] = (unsigned long long)item; trp[1] = gtime(); }
@@ -670,7 +742,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             __stcg(slice + (c / 4 + j / 4) * 32 + lane,
                    make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
                                __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3])));
-        } else {
+        } else if (!(p.debug & 2)) {
           float f[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
@@ -832,6 +904,9 @@ static std::atomic<int> g_pair{1};
 static std::atomic<int> g_max_ctas{0};
 static std::atomic<int> g_split_k{1};
 static std::atomic<int> g_pdl{0};
+static std::atomic<int> g_raster{0};
+static std::atomic<int> g_epi_sleep{1};
+static std::atomic<int> g_debug{0};
 static unsigned long long *g_trace = nullptr;
 static std::atomic<unsigned long long> g_split_window_ns{250000};
 
@@ -892,7 +967,8 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
   constexpr int BNC = BN / kPair;
   CUtensorMap ma, mb, mc, mh;
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-  const auto SW = CU_TENSOR_MAP_SWIZZLE_128B, NOSW = CU_TENSOR_MAP_SWIZZLE_NONE;
+  // operands: SWIZZLE_128B; staged output boxes: 128B (fp32) / 64B (bf16) swizzle
+  const auto SW = CU_TENSOR_MAP_SWIZZLE_128B, SW64 = CU_TENSOR_MAP_SWIZZLE_64B;
   int st;
   // A is logically [M x K]: K-major stored [M][lda], MN-major stored [K][lda]
   if ((st = a_mn ? make_map(&ma, A, BF, 2, p.M, p.K, lda, 64, BK, SW)
@@ -917,7 +993,7 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
       if (p.red_base[i] &&
           make_map(&pm.m[i], p.red_base[i],
                    p.c_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : BF, ce, p.N, 1ll << 24, p.red_ld,
-                   32, 32, NOSW))
+                   32, 32, p.c_f32 ? SW : SW64))
         ok = false;
     if (!ok) p.push_tma = p.tma_red = 0;  // unaligned peer copy: per-row stores / red.add
   }
@@ -926,10 +1002,10 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
   memset(&mc, 0, sizeof mc);
   memset(&mh, 0, sizeof mh);
   if (p.c_tma && (st = p.c_f32 ? make_map(&mc, C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.N, p.M, ldc,
-                                          32, 32, NOSW)
-                               : make_map(&mc, C, BF, 2, p.N, p.M, ldc, 32, 32, NOSW)))
+                                          32, 32, SW)
+                               : make_map(&mc, C, BF, 2, p.N, p.M, ldc, 32, 32, SW64)))
     return st;
-  if (p.h_tma && (st = make_map(&mh, H, BF, 2, p.N, p.M, ldh, 32, 32, NOSW))) return st;
+  if (p.h_tma && (st = make_map(&mh, H, BF, 2, p.N, p.M, ldh, 32, 32, SW64))) return st;
   auto kern = gemm_kernel<BN, kPair, kStg>;
   const int smem = (int)sizeof(Smem<BN, kPair, kStg>) + 1024;
   static std::once_flag once[64];
@@ -952,6 +1028,9 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
   p.tile_cnt = nullptr;
   p.ws = nullptr;
   p.trace = g_trace;
+  p.raster = g_raster.load();
+  p.epi_sleep = g_epi_sleep.load();
+  p.debug = g_debug.load();
   p.split_window_ns = g_split_window_ns.load();
   const int rem = tiles % units, nkb = (p.K + BK - 1) / BK;
   if (g_split_k.load() && rem > 0) {
@@ -1127,6 +1206,26 @@ extern "C" int ntp_gemm_set_split_k(int on) {
 // 250 us; 0 forces the last-arrival path).
 extern "C" int ntp_gemm_debug_split_window(unsigned long long ns) {
   gemm::g_split_window_ns.store(ns);
+  return NTP_OK;
+}
+
+// Debug hook, not in the header: tile order (groups of n M-tile rows; 0 = all)
+extern "C" int ntp_gemm_debug_raster(int n) {
+  if (n < 0) return fail(NTP_EINVAL, "bad raster group");
+  gemm::g_raster.store(n);
+  return NTP_OK;
+}
+
+// Debug hook, not in the header: 1 (default) the epilogue's accumulator wait
+// sleeps between polls; 0 spins
+extern "C" int ntp_gemm_debug_epi_sleep(int on) {
+  gemm::g_epi_sleep.store(on ? 1 : 0);
+  return NTP_OK;
+}
+
+// Debug hook, not in the header: experiment bits (1 no loads, 2 no epilogue output)
+extern "C" int ntp_gemm_debug_mode(int bits) {
+  gemm::g_debug.store(bits);
   return NTP_OK;
 }
 
