@@ -187,6 +187,10 @@ struct Params {
   // debug only (ntp_gemm_debug_trace): per (CTA, local item) 8 u64:
   // {item, t_full, t_done, t_kernel_start, t_prod_first, t_prod_last, t_mma_first, t_mma_last}
   unsigned long long *trace;
+  // debug only (ntp_gemm_debug_counters): per leader CTA 4 u64 of clock64
+  // cycles: {-, MMA waiting for full stages, MMA waiting for a free
+  // accumulator, MMA loop total}
+  unsigned long long *counters;
   // EPI_PUSH with push_tma = 1: a 32-row box whose rows map to consecutive rows
   // of one peer copy goes there as one TMA tensor store (peer_maps[pb]) from the
   // same smem staging as the local store; other boxes fall back to row stores
@@ -397,7 +401,8 @@ __device__ __forceinline__ void tc_commit2(uint64_t *bar, uint16_t mask) {
 // MMAs of tile i+1.  kPair = 2: a CTA pair (cluster of 2) computes a 256 x BN
 // tile with tcgen05.mma.cta_group::2 -- each CTA stages its 128 rows of A and
 // half of B, the leader issues the MMAs, both drain their own TMEM half.
-template <int BN, int kPair, int kStg>
+// kEpi: the fused epilogue, one instantiation each (see launch()).
+template <int BN, int kPair, int kStg, int kEpi>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
             const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_h,
@@ -455,8 +460,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   if (p.trace && threadIdx.x == 0) p.trace[(size_t)blockIdx.x * kTraceItems * 8 + 3] = gtime();
 
   if (warp == 0) {
-    if (lane == 0) {
+    {
       // ---- TMA producer (both CTAs of a pair) ----
+      // The whole warp walks the schedule (warp-uniform values stay in uniform
+      // registers, which the TMA instructions take) and one elected lane issues.
       const uint32_t cta_bytes = (BM + BNC) * BK * 2;
       int it = 0, plocal = 0;
       for (int item = unit_id; item < num_items && !(p.debug & 8); item += num_units, ++plocal) {
@@ -467,34 +474,38 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         const int m0 = tm * TM + (int)rank * BM;
         const int n0 = tn * BN + (int)rank * BNC;
         unsigned long long *trp =
-            p.trace && plocal < kTraceItems ? p.trace + ((size_t)blockIdx.x * kTraceItems + plocal) * 8 : nullptr;
+            p.trace && lane == 0 && plocal < kTraceItems ? p.trace + ((size_t)blockIdx.x * kTraceItems + plocal) * 8 : nullptr;
         for (int kb = w.kb_lo; kb < w.kb_hi; ++kb, ++it) {
           const int s = it % kStg;
           mbar_wait(&sm.empty[s], ((it / kStg) & 1) ^ 1);
           if (trp && kb == w.kb_lo) trp[4] = gtime();
           if (trp && kb == w.kb_hi - 1) trp[5] = gtime();
           if (p.debug & 1) {  // debug: no operand loads (MMA ceiling on stale smem)
-            if (leader) mbar_arrive(&sm.full[s]);
+            if (leader && lane == 0) mbar_arrive(&sm.full[s]);
+            __syncwarp();
             continue;
           }
-          if (leader) mbar_expect_tx(&sm.full[s], cta_bytes * kPair);
-          const int k0 = kb * BK;
-          auto load = [&](void *dst, const CUtensorMap *m, int c0, int c1) {
-            if constexpr (kPair == 2) tma_load_2d_pair(dst, m, c0, c1, &sm.full[s]);
-            else tma_load_2d(dst, m, c0, c1, &sm.full[s]);
-          };
-          if (!p.a_mn) {
-            load(sm.a[s], &map_a, k0, m0);
-          } else {
+          if (elect_one()) {
+            if (leader) mbar_expect_tx(&sm.full[s], cta_bytes * kPair);
+            const int k0 = kb * BK;
+            auto load = [&](void *dst, const CUtensorMap *m, int c0, int c1) {
+              if constexpr (kPair == 2) tma_load_2d_pair(dst, m, c0, c1, &sm.full[s]);
+              else tma_load_2d(dst, m, c0, c1, &sm.full[s]);
+            };
+            if (!p.a_mn) {
+              load(sm.a[s], &map_a, k0, m0);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) load(sm.a[s] + j * 64 * BK, &map_a, m0 + 64 * j, k0);
-          }
-          if (!p.b_mn) {
-            load(sm.b[s], &map_b, k0, n0);
-          } else {
+              for (int j = 0; j < BM / 64; ++j) load(sm.a[s] + j * 64 * BK, &map_a, m0 + 64 * j, k0);
+            }
+            if (!p.b_mn) {
+              load(sm.b[s], &map_b, k0, n0);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BNC / 64; ++j) load(sm.b[s] + j * 64 * BK, &map_b, n0 + 64 * j, k0);
+              for (int j = 0; j < BNC / 64; ++j) load(sm.b[s] + j * 64 * BK, &map_b, n0 + 64 * j, k0);
+            }
           }
+          __syncwarp();
         }
       }
     }
@@ -514,17 +525,31 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       const uint64_t bd0 = smem_desc(smem_u32(sm.b[0]), b_lbo, 1024);
       constexpr uint32_t a_stage16 = (BM * BK * 2) >> 4, b_stage16 = (BNC * BK * 2) >> 4;
       int it = 0, local = 0;
+      long long cnt_full = 0, cnt_acc = 0;
+      const long long c_start = p.counters ? clock64() : 0;
       for (int item = unit_id; item < num_items; item += num_units, ++local) {
         const Work w = decode_work(item, p, nk);
         const int acc = local & 1;
-        mbar_wait(&sm.tmem_empty[acc], ((local >> 1) & 1) ^ 1);
+        if (p.counters) {
+          const long long c0 = clock64();
+          mbar_wait(&sm.tmem_empty[acc], ((local >> 1) & 1) ^ 1);
+          cnt_acc += clock64() - c0;
+        } else {
+          mbar_wait(&sm.tmem_empty[acc], ((local >> 1) & 1) ^ 1);
+        }
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(acc * BN);
         unsigned long long *trp =
             p.trace && lane == 0 && local < kTraceItems ? p.trace + ((size_t)blockIdx.x * kTraceItems + local) * 8 : nullptr;
         for (int kb = w.kb_lo; kb < w.kb_hi; ++kb, ++it) {
           const int s = it % kStg;
-          if (!(p.debug & 4)) mbar_wait(&sm.full[s], (it / kStg) & 1);
+          if (p.counters) {
+            const long long c0 = clock64();
+            mbar_wait(&sm.full[s], (it / kStg) & 1);
+            cnt_full += clock64() - c0;
+          } else if (!(p.debug & 4)) {
+            mbar_wait(&sm.full[s], (it / kStg) & 1);
+          }
           if (trp && kb == w.kb_lo) trp[6] = gtime();
           if (trp && kb == w.kb_hi - 1) trp[7] = gtime();
           tc_fence_after();
@@ -550,6 +575,12 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         }
         __syncwarp();
       }
+      if (p.counters && lane == 0) {
+        unsigned long long *c = p.counters + (size_t)blockIdx.x * 4;
+        c[1] = (unsigned long long)cnt_full;
+        c[2] = (unsigned long long)cnt_acc;
+        c[3] = (unsigned long long)(clock64() - c_start);
+      }
     }
   } else {
     // ---- epilogue: TMEM -> registers -> fused op -> smem -> TMA store ----
@@ -564,7 +595,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         if (col0 >= p.N || row0 >= p.M) return;  // warp-uniform: nothing of this box is stored
 #pragma unroll
         for (int j = 0; j < 32; ++j) f[j] *= p.alpha;
-        if ((p.epi == EPI_RED && !p.tma_red) || (p.epi == EPI_PUSH && !p.push_tma)) {
+        if ((kEpi == EPI_RED && !p.tma_red) || (kEpi == EPI_PUSH && !p.push_tma)) {
           // fused sync: this replica's weighted contribution goes into its own copy
           // and, over NVLink, into the partner replica's copy (EPI_RED: red.add
           // into zeroed arenas) or the partner's staging arena (EPI_PUSH: plain
@@ -576,7 +607,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             const int pb = p.red_buf[row];
             char *peer = pb >= 0 ? p.red_base[pb] + ((long long)p.red_row[row] * p.red_ld + col0) * ce
                                  : nullptr;
-            if (p.epi == EPI_RED) {
+            if (kEpi == EPI_RED) {
               red_row32(own, f, p.c_f32);
               if (peer) red_row32(peer, f, p.c_f32);
             } else {
@@ -592,7 +623,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         sbuf ^= 1;
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         __syncwarp();
-        if (p.epi == EPI_GELU) {
+        if (kEpi == EPI_GELU) {
           // H = bf16(acc) (kept for the backward), Y = GeLU(H)
           uint4 *hs = reinterpret_cast<uint4 *>(stage + 2048 + lane * 64);
           uint4 *ys = reinterpret_cast<uint4 *>(stage + lane * 64);
@@ -612,7 +643,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             ys[(j / 8) ^ sw] = make_uint4(yw[0], yw[1], yw[2], yw[3]);
           }
         } else {
-          if (p.epi == EPI_DGELU && row < p.M) {
+          if (kEpi == EPI_DGELU && row < p.M) {
             const __nv_bfloat16 *h = p.aux + (long long)row * p.ld_aux + col0;
             const int nc = min(32, p.N - col0);
             if (nc == 32 && !(reinterpret_cast<uintptr_t>(h) & 15u)) {
@@ -660,8 +691,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         // -- one TMA store over NVLink when its 32 rows are consecutive rows of
         // one peer copy, else row stores from registers (run boundaries, ragged M)
         int peer_box = -1, peer_row0 = 0;
-        const bool reduce = p.epi == EPI_RED;  // only reached with tma_red
-        if (p.epi == EPI_PUSH || reduce) {
+        const bool reduce = kEpi == EPI_RED;  // only reached with tma_red
+        if (kEpi == EPI_PUSH || reduce) {
           const int pb = row < p.M ? p.red_buf[row] : -1;
           const int pr = row < p.M ? p.red_row[row] : 0;
           const int pb0 = __shfl_sync(0xffffffffu, pb, 0), pr0 = __shfl_sync(0xffffffffu, pr, 0);
@@ -681,13 +712,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             if (peer_box >= 0) tma_reduce_add_2d(&peer_maps.m[peer_box], stage, col0, peer_row0);
           } else {
             if (p.c_tma) tma_store_2d(&map_c, stage, col0, row0);  // TMA clips rows >= M, cols >= N
-            if (p.epi == EPI_GELU && p.h_tma) tma_store_2d(&map_h, stage + 2048, col0, row0);
+            if (kEpi == EPI_GELU && p.h_tma) tma_store_2d(&map_h, stage + 2048, col0, row0);
             if (peer_box >= 0) tma_store_2d(&peer_maps.m[peer_box], stage, col0, peer_row0);
           }
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
         if (!p.c_tma) box_store(stage, p.C, p.ldc, p.c_f32 ? 4 : 2, row0, col0, p.M, p.N, lane);
-        if (p.epi == EPI_GELU && !p.h_tma)
+        if (kEpi == EPI_GELU && !p.h_tma)
           box_store(stage + 2048, p.H, p.ldh, 2, row0, col0, p.M, p.N, lane);
         __syncwarp();
     };
@@ -866,6 +897,8 @@ static EncodeFn encode_fn() {
 
 // 2-D tensor map over a row-major [outer][ld] array with logical inner extent
 // `inner`: box {box_inner, box_outer}.
+static std::atomic<int> g_l2promo{3};
+
 static int make_map(CUtensorMap *m, const void *ptr, CUtensorMapDataType dt, int esize,
                     long long inner, long long outer, long long ld, int box_inner, int box_outer,
                     CUtensorMapSwizzle swz) {
@@ -878,7 +911,7 @@ static int make_map(CUtensorMap *m, const void *ptr, CUtensorMapDataType dt, int
   cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
   cuuint32_t es[2] = {1u, 1u};
   CUresult r = enc(m, dt, 2, const_cast<void *>(ptr), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, (CUtensorMapL2promotion)g_l2promo.load(),
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     char b[96];
@@ -908,6 +941,7 @@ static std::atomic<int> g_raster{0};
 static std::atomic<int> g_epi_sleep{1};
 static std::atomic<int> g_debug{0};
 static unsigned long long *g_trace = nullptr;
+static unsigned long long *g_counters = nullptr;
 static std::atomic<unsigned long long> g_split_window_ns{250000};
 
 // Split-K partials and per-slice arrival counters, one set per (device, stream)
@@ -1006,12 +1040,23 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
                                : make_map(&mc, C, BF, 2, p.N, p.M, ldc, 32, 32, SW64)))
     return st;
   if (p.h_tma && (st = make_map(&mh, H, BF, 2, p.N, p.M, ldh, 32, 32, SW64))) return st;
-  auto kern = gemm_kernel<BN, kPair, kStg>;
+  // one kernel per (producer style, epilogue): each instantiation carries only
+  // its own epilogue, which keeps the kernel's code within the instruction cache
+  // (measured: the all-epilogue kernel, ~150 KB of SASS, slowed the fused-GeLU
+  // GEMMs by 10-15 %)
+  using Kern = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
+                        const PeerMaps, Params);
+  static const Kern table[5] = {
+      gemm_kernel<BN, kPair, kStg, EPI_NONE>, gemm_kernel<BN, kPair, kStg, EPI_GELU>,
+      gemm_kernel<BN, kPair, kStg, EPI_DGELU>, gemm_kernel<BN, kPair, kStg, EPI_RED>,
+      gemm_kernel<BN, kPair, kStg, EPI_PUSH>};
+  if (p.epi < 0 || p.epi > EPI_PUSH) return fail(NTP_EINVAL, "unknown GEMM epilogue");
+  auto kern = table[p.epi];
   const int smem = (int)sizeof(Smem<BN, kPair, kStg>) + 1024;
-  static std::once_flag once[64];
+  static std::once_flag once[5][64];
   int dev = 0;
   cudaGetDevice(&dev);
-  std::call_once(once[dev & 63], [&] {
+  std::call_once(once[p.epi][dev & 63], [&] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   });
   p.num_m = (p.M + BM * kPair - 1) / (BM * kPair);
@@ -1028,6 +1073,7 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
   p.tile_cnt = nullptr;
   p.ws = nullptr;
   p.trace = g_trace;
+  p.counters = g_counters;
   p.raster = g_raster.load();
   p.epi_sleep = g_epi_sleep.load();
   p.debug = g_debug.load();
@@ -1224,8 +1270,23 @@ extern "C" int ntp_gemm_debug_epi_sleep(int on) {
 }
 
 // Debug hook, not in the header: experiment bits (1 no loads, 2 no epilogue output)
+// Debug hook, not in the header: TMA L2 promotion of the GEMM maps (0 none,
+// 1 64B, 2 128B, 3 256B = default)
+extern "C" int ntp_gemm_debug_l2promo(int v) {
+  if (v < 0 || v > 3) return fail(NTP_EINVAL, "bad L2 promotion");
+  gemm::g_l2promo.store(v);
+  return NTP_OK;
+}
+
 extern "C" int ntp_gemm_debug_mode(int bits) {
   gemm::g_debug.store(bits);
+  return NTP_OK;
+}
+
+// Debug hook, not in the header: device buffer of gridDim * 4 u64 receiving
+// per-CTA wait-cycle counters (nullptr: off)
+extern "C" int ntp_gemm_debug_counters(void *buf) {
+  gemm::g_counters = static_cast<unsigned long long *>(buf);
   return NTP_OK;
 }
 

@@ -1,3 +1,9 @@
+"""Summarise scripts/gpu_gemm_ab.sh captures (ncu --clock-control base): per
+GEMM kind, ours / cuBLAS in kilo-cycles (duration x SM clock, so boxes with
+different base clocks compare) and tensor-pipe active %.
+
+    python scripts/gemm_ab_summary.py gpurun_out/ab
+"""
 import csv,glob,collections,sys,statistics
 for f in sorted(glob.glob(sys.argv[1]+'/*.csv')):
     rows=[r for r in csv.reader(l for l in open(f) if l.startswith('"'))]
