@@ -359,14 +359,38 @@ def main(argv=None):
             print(json.dumps(out), flush=True)
         return 0
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
-        from paper_2504_06095_b200 import dist_bench
-        out = dist_bench.run(args)
-    else:
-        out = run_single(args)
+    with _stdout_to_stderr():  # library banners (NCCL's version line) stay off stdout
+        if world > 1 or args.gpus > 1:
+            from paper_2504_06095_b200 import dist_bench
+            out = dist_bench.run(args)
+        else:
+            out = run_single(args)
     if out is not None:
         print(json.dumps(out), flush=True)
     return 0
+
+
+class _stdout_to_stderr:
+    """Point fd 1 at stderr while the benchmark runs, so the only thing on
+    stdout is the JSON line printed after it (NCCL prints its version banner
+    with printf at NCCL_DEBUG=WARN/VERSION)."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        try:
+            import ctypes
+            ctypes.CDLL(None).fflush(None)
+        except OSError:
+            pass
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+        return False
 
 
 if __name__ == "__main__":

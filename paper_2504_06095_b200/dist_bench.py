@@ -30,10 +30,9 @@ def _max(x: float) -> float:
 def run(args):
     from bench import METRIC, W_H, W_R, ClockSampler, peaks  # noqa: I001 (repo root on sys.path)
 
-    # stdout carries exactly one JSON line: NCCL's own messages (its version
-    # banner prints at NCCL_DEBUG >= VERSION) go to a per-process file instead
+    # NCCL warnings (and its version banner) go to stderr: bench.py keeps fd 1
+    # pointed at stderr while this runs, so stdout is the one JSON line
     os.environ["NCCL_DEBUG"] = os.environ.get("NTP_NCCL_DEBUG", os.environ.get("NCCL_DEBUG", "WARN"))
-    os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/ntp_nccl.%h.%p.log")
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if not dist.is_initialized():
