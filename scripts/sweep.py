@@ -1,12 +1,12 @@
 """BASELINE configs[4]: grad-sync message-size sweep (1 MB .. 1 GB per replica)
 and TP4 -> TP3 / TP4 -> TP2 reconfiguration of an 8B-shaped parameter set.
 
-Single process.  With one GPU every logical rank is a buffer on cuda:0 (HBM
-roofline); under torchrun with 2+ ranks the sync sweep uses the NVLink push
-path (dist.NtpSyncGroup).  Prints one JSON document.
+With one GPU every logical rank is a buffer on cuda:0 (HBM roofline); under
+torchrun with 2+ ranks the sync sweep runs across the GPUs over NVLink
+(dist.NtpSyncGroup, the bench's N>1 path).  Prints one JSON document.
 
     python scripts/sweep.py [--reconfig-layers L]
-    torchrun --nproc-per-node 2 scripts/sweep.py --sync-only
+    torchrun --nproc-per-node N scripts/sweep.py
 """
 
 import argparse
@@ -104,13 +104,81 @@ def reconfig(layers):
     return out
 
 
+def sync_sweep_dist():
+    """The same message sizes across processes (torchrun, one per GPU): the 7
+    logical ranks placed by Placement.default, NVLink peer-memory sync
+    (dist.NtpSyncGroup, the bench's N>1 path), device-timed, max over ranks.
+    At N=2 NCCL's all-reduce of one replica's bytes between the two GPUs (what a
+    uniform DP=2 sync moves) is timed beside it."""
+    import torch.distributed as dist
+    from paper_2504_06095_b200.dist import NtpSyncGroup, Placement
+    from paper_2504_06095_b200.dist_bench import busiest_bytes_for
+    rank, world = dist.get_rank(), dist.get_world_size()
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    def dmax(x):
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def dtimed(fn, iters):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return dmax(e0.elapsed_time(e1) / iters)
+
+    rows = []
+    for mb in (1, 4, 16, 64, 256, 1024):
+        k = max(8, mb * 2**20 // (2 * 4096 * 2))
+        lay = pair_layout(ModelShape(f"sweep{mb}", 4096, k, 0, 1), 4, 3)
+        plc = Placement.default(world, 4, 3)
+        grp = NtpSyncGroup(lay, plc, torch.bfloat16, device=local).upload()
+        for s in grp.hosted:
+            a = grp.arena(s)
+            a.copy_(torch.randn(a.numel(), device="cuda").to(torch.bfloat16))
+        iters = max(5, min(500, int(2e9 / (lay.elems * 2))))
+        ms = dtimed(lambda: grp.step(4 / 7, 3 / 7), iters)
+        if grp.status() != 0:
+            raise RuntimeError(f"rank {rank}: signal timeout")
+        B = busiest_bytes_for(lay, plc, 2)
+        row = {"grad_bytes_per_replica": lay.elems * 2, "k": k, "us": round(ms * 1e3, 2),
+               "busiest_gpu_bytes_per_direction": B,
+               "nvlink_gbs": round(B / ms / 1e6, 1), "frac_nvlink": round(B / ms / 1e6 / NVL, 3)}
+        if world == 2:
+            t = torch.randn(lay.elems, device="cuda").to(torch.bfloat16)
+            ms_n = dtimed(lambda: dist.all_reduce(t), iters)
+            row["nccl_allreduce_us"] = round(ms_n * 1e3, 2)
+            del t
+        rows.append(row)
+        dist.barrier()
+        grp.close()
+    return rows
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reconfig-layers", type=int, default=32)
     ap.add_argument("--sync-only", action="store_true")
     args = ap.parse_args()
     _lib.load()
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        rows = sync_sweep_dist()
+        if dist.get_rank() == 0:
+            print(json.dumps({"device": torch.cuda.get_device_name(), "n_gpus": dist.get_world_size(),
+                              f"sync_sweep_{dist.get_world_size()}gpu": rows}, indent=1))
+        dist.destroy_process_group()
+        return
     doc = {"device": torch.cuda.get_device_name(), "sync_sweep_1gpu": sync_sweep_local()}
     if not args.sync_only:
         doc["reconfig_8b_1gpu"] = reconfig(args.reconfig_layers)
