@@ -314,6 +314,21 @@ int ntp_grad_sync_signaled(const ntp_plan *plan, void *const *bufs, int n_bufs, 
                            uint64_t *const *post, int n_post, uint64_t epoch,
                            uint64_t spin_ns, int *status, void *stream);
 
+/* One whole synchronisation step in a single launch (the three launches of
+ * ntp_signal_post + ntp_grad_sync_signaled + ntp_signal_wait folded together):
+ * post epoch to post_ready[] (this process's buffers may be touched), wait for
+ * wait_ready[], run the plan, post post_done[] after every CTA has finished,
+ * then wait for wait_done[] (the partners finished touching this process's
+ * buffers) before the launch completes.  plan may be NULL (nothing to compute
+ * here: only the handshakes run).  Replaces one call of the reference's
+ * nonuniform_grad_sync (tpnumerics.py:289-356) across processes. */
+int ntp_grad_sync_step(const ntp_plan *plan, void *const *bufs, int n_bufs, int op, double w_a,
+                       double w_b, uint64_t *const *post_ready, int n_post_ready,
+                       uint64_t *const *wait_ready, int n_wait_ready,
+                       uint64_t *const *post_done, int n_post_done,
+                       uint64_t *const *wait_done, int n_wait_done, uint64_t epoch,
+                       uint64_t spin_ns, int *status, void *stream);
+
 /* Store epoch to each word in post[] (release, .sys) from a 1-thread kernel. */
 int ntp_signal_post(uint64_t *const *post, int n_post, uint64_t epoch, void *stream);
 

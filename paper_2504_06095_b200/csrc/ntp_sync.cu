@@ -53,6 +53,12 @@ struct SignalArgs {
   uint64_t *wait[16];
   uint64_t *post[16];
   int n_wait, n_post;
+  // single-launch step (ntp_grad_sync_step): `pre` words are posted before the
+  // wait (this process's "ready"), `fin` words are waited for after the post
+  // (the partners' "done"); both empty for ntp_grad_sync_signaled
+  uint64_t *pre[16];
+  uint64_t *fin[16];
+  int n_pre, n_fin;
   uint64_t epoch;
   uint64_t spin_ns;
   int *status;
@@ -206,12 +212,34 @@ __device__ bool wait_signals(uint64_t *const *wait, int n, uint64_t epoch, uint6
 // ---------------------------------------------------------------------------
 // the plan kernels
 
+__device__ __forceinline__ void post_signals(uint64_t *const *post, int n, uint64_t epoch) {
+  if (n == 0) return;
+  __threadfence_system();
+  for (int i = 0; i < n; ++i) st_release_sys(post[i], epoch);
+}
+
+// Last CTA of a signalled launch: every CTA's stores are fenced -- post the
+// done words, then (single-launch step) wait for the partners' done words.
+__device__ __forceinline__ void last_cta_finish(const SignalArgs &sig) {
+  __threadfence_system();
+  *sig.counter = 0u;
+  for (int i = 0; i < sig.n_post; ++i) st_release_sys(sig.post[i], sig.epoch);
+  if (sig.n_fin) wait_signals(sig.fin, sig.n_fin, sig.epoch, sig.spin_ns, sig.status);
+}
+
 template <bool kSignaled>
 __device__ __forceinline__ bool cta_prologue(const SignalArgs &sig) {
   if constexpr (kSignaled) {
     __shared__ int ok;
-    if (threadIdx.x == 0)
+    if (threadIdx.x == 0) {
+      // the first CTA to start posts this process's ready words, so no CTA
+      // waits on a post that an unscheduled CTA would make (word 1 of the
+      // plan's counter block records the last epoch posted)
+      if (sig.n_pre && atomicMax(reinterpret_cast<unsigned long long *>(sig.counter) + 1,
+                                 (unsigned long long)sig.epoch) < sig.epoch)
+        post_signals(sig.pre, sig.n_pre, sig.epoch);
       ok = wait_signals(sig.wait, sig.n_wait, sig.epoch, sig.spin_ns, sig.status) ? 1 : 0;
+    }
     __syncthreads();
     return ok != 0;
   } else {
@@ -226,11 +254,7 @@ __device__ __forceinline__ void cta_epilogue(const SignalArgs &sig) {
     __syncthreads();
     if (threadIdx.x == 0) {
       const unsigned int done = atomicAdd(sig.counter, 1u);
-      if (done == gridDim.x - 1) {  // last CTA: every CTA's stores are fenced
-        __threadfence_system();
-        *sig.counter = 0u;
-        for (int i = 0; i < sig.n_post; ++i) st_release_sys(sig.post[i], sig.epoch);
-      }
+      if (done == gridDim.x - 1) last_cta_finish(sig);  // every CTA's stores are fenced
     }
   }
 }
@@ -428,11 +452,7 @@ plan_kernel_bulk(const Chunk *__restrict__ chunks, int n_chunks, BufTable bufs,
       asm volatile("fence.proxy.async.global;" ::: "memory");
       __threadfence_system();
       const unsigned int done = atomicAdd(sig.counter, 1u);
-      if (done == gridDim.x - 1) {
-        __threadfence_system();
-        *sig.counter = 0u;
-        for (int i = 0; i < sig.n_post; ++i) st_release_sys(sig.post[i], sig.epoch);
-      }
+      if (done == gridDim.x - 1) last_cta_finish(sig);
     }
   }
 }
@@ -494,6 +514,15 @@ __global__ void signal_post_kernel(SignalArgs sig) {
 
 __global__ void signal_wait_kernel(SignalArgs sig) {
   wait_signals(sig.wait, sig.n_wait, sig.epoch, sig.spin_ns, sig.status);
+}
+
+// a step with nothing to compute: post ready, wait ready, post done, wait done
+__global__ void signal_step_kernel(SignalArgs sig) {
+  post_signals(sig.pre, sig.n_pre, sig.epoch);
+  if (wait_signals(sig.wait, sig.n_wait, sig.epoch, sig.spin_ns, sig.status)) {
+    post_signals(sig.post, sig.n_post, sig.epoch);
+    wait_signals(sig.fin, sig.n_fin, sig.epoch, sig.spin_ns, sig.status);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -829,6 +858,38 @@ int ntp_grad_sync_signaled(const ntp_plan *p, void *const *bufs, int n_bufs, int
     st = launch_plan<true>(p, op, bt, w_a, w_b, sig, s);
     if (st) return st;
   }
+  NTP_CUDA(cudaGetLastError());
+  return NTP_OK;
+}
+
+int ntp_grad_sync_step(const ntp_plan *p, void *const *bufs, int n_bufs, int op, double w_a,
+                       double w_b, uint64_t *const *post_ready, int n_post_ready,
+                       uint64_t *const *wait_ready, int n_wait_ready, uint64_t *const *post_done,
+                       int n_post_done, uint64_t *const *wait_done, int n_wait_done,
+                       uint64_t epoch, uint64_t spin_ns, int *status, void *stream) {
+  if (n_post_ready < 0 || n_post_ready > 16 || n_wait_done < 0 || n_wait_done > 16)
+    return fail(NTP_EINVAL, "at most 16 wait and 16 post signals");
+  SignalArgs sig;
+  int st = fill_signals(sig, wait_ready, n_wait_ready, post_done, n_post_done, epoch, spin_ns,
+                        status);
+  if (st) return st;
+  for (int i = 0; i < n_post_ready; ++i) sig.pre[i] = post_ready[i];
+  for (int i = 0; i < n_wait_done; ++i) sig.fin[i] = wait_done[i];
+  sig.n_pre = n_post_ready;
+  sig.n_fin = n_wait_done;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!p || p->chunks.empty()) {
+    if (p && (st = set_device(p->device))) return st;
+    signal_step_kernel<<<1, 1, 0, s>>>(sig);
+    NTP_CUDA(cudaGetLastError());
+    return NTP_OK;
+  }
+  BufTable bt;
+  if ((st = check_exec(p, bufs, n_bufs, bt))) return st;
+  if (op < NTP_OP_SUM || op > NTP_OP_WEIGHTED) return fail(NTP_EINVAL, "unknown reduction op");
+  if ((st = set_device(p->device))) return st;
+  sig.counter = p->d_counter;
+  if ((st = launch_plan<true>(p, op, bt, w_a, w_b, sig, s))) return st;
   NTP_CUDA(cudaGetLastError());
   return NTP_OK;
 }

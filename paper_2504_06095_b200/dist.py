@@ -271,6 +271,10 @@ class NtpSyncGroup:
         self.wait_done = [self.sig + 8 * (DONE * SIG_WORDS + p) for p in self.partners]
         self.epoch = 0
         self._status = None
+        # True: step() is one launch (ntp_grad_sync_step); False: three launches
+        # (post ready / signalled sync / wait done), kept for comparison
+        self.fused_step = True
+        self._sig_arrays = None
 
     def _build_plans(self, policy) -> None:
         """What this process computes under an executor policy, which peer
@@ -359,6 +363,20 @@ class NtpSyncGroup:
         s = torch.cuda.current_stream(self.device) if stream is None else stream
         sp = ctypes.c_void_p(s.cuda_stream)
         st = ctypes.cast(self._status.data_ptr(), ctypes.POINTER(ctypes.c_int))
+        if self.fused_step and self.partners:
+            # one launch: post ready, wait ready, sync, post done, wait done
+            if self._sig_arrays is None:
+                self._sig_arrays = tuple(_lib.u64_ptr_array(w) for w in
+                                         (self.post_ready, self.wait_ready, self.post_done,
+                                          self.wait_done))
+            pr, wr, pd, wd = self._sig_arrays
+            bufs = _lib.ptr_array(self.bufs)
+            _lib.check(L.ntp_grad_sync_step(
+                plan._h if plan is not None else None, bufs, len(self.bufs), OPS["weighted"],
+                float(w_h), float(w_r), pr, len(self.post_ready), wr, len(self.wait_ready),
+                pd, len(self.post_done), wd, len(self.wait_done), e, int(spin_ns), st, sp),
+                "ntp_grad_sync_step")
+            return
         if self.post_ready:
             _lib.check(L.ntp_signal_post(_lib.u64_ptr_array(self.post_ready), len(self.post_ready),
                                          e, sp), "ntp_signal_post")

@@ -135,8 +135,12 @@ def busiest_bytes_for(lay, plc: Placement, eb: int) -> int:
     return worst * eb
 
 
-def _launches_per_step(grp) -> int:
-    return int(grp.plan is not None) + int(bool(grp.post_ready)) + int(bool(grp.wait_done))
+def _launches_per_step(grp, plan="whole") -> int:
+    """Kernels one step() launches on this rank (see NtpSyncGroup.step)."""
+    p = grp.plan if plan == "whole" else plan
+    if grp.partners and grp.fused_step:
+        return 1
+    return int(p is not None) + int(bool(grp.post_ready)) + int(bool(grp.wait_done))
 
 
 def run_e2e(args, grp, lay, dtype, eb):
@@ -212,6 +216,5 @@ def run_e2e(args, grp, lay, dtype, eb):
             "pipeline_pieces": len(ranges),
             "host_copies_only_ms": round(copy_ms, 3),
             "host_link_frac": round(copy_ms / ms, 3),
-            "gpu_launches_per_step": sum(int(p is not None) for p in grp.piece_plans)
-                                     + len(ranges) * (int(bool(grp.post_ready)) + int(bool(grp.wait_done))),
+            "gpu_launches_per_step": sum(_launches_per_step(grp, p) for p in grp.piece_plans),
             "wall_ms_per_step": round(wall_ms, 3)}
