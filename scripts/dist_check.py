@@ -2,7 +2,12 @@
 arenas through NtpSyncGroup (IPC peer memory + device signals); rank 0 gathers
 all arenas and compares them with the oracle's fp64 nonuniform sync.
 
-    torchrun --nproc-per-node N scripts/dist_check.py [n1 n2 dtype steps]
+    torchrun --nproc-per-node N scripts/dist_check.py [n1 n2 dtype steps [launch [policy]]]
+
+launch: "fused" (default, one ntp_grad_sync_step per step), "three" (post ready /
+signalled sync / wait done) or "alternate"; policy: the executor policy
+("split" default, "healthy": the reduced side computes nothing and only
+hand-shakes)
 """
 
 import os
@@ -27,6 +32,8 @@ def main():
     n2 = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     dname = sys.argv[3] if len(sys.argv) > 3 else "f32"
     steps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
+    launch = sys.argv[5] if len(sys.argv) > 5 else "fused"
+    policy = sys.argv[6] if len(sys.argv) > 6 else "split"
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -35,7 +42,7 @@ def main():
     lay = pair_layout(shape, n1, n2)
     plc = Placement.default(world, n1, n2)
     dtype = DT[dname]
-    grp = NtpSyncGroup(lay, plc, dtype, device=local).upload()
+    grp = NtpSyncGroup(lay, plc, dtype, device=local, policy=policy).upload()
     rng = np.random.default_rng(0)
     init = [rng.standard_normal(e) for e in list(lay.h_elems) + list(lay.r_elems)]
     init = [torch.from_numpy(a).to(dtype).double().numpy() for a in init]  # representable
@@ -44,7 +51,8 @@ def main():
     torch.cuda.synchronize()
     dist.barrier()
     w = (4 / 7, 3 / 7)
-    for _ in range(steps):
+    for i in range(steps):
+        grp.fused_step = launch == "fused" or (launch == "alternate" and i % 2 == 0)
         grp.step(*w)
     torch.cuda.synchronize()
     dist.barrier()
@@ -81,7 +89,7 @@ def main():
             worst = max(worst, err)
         ok = worst <= max(TOL[dname], 0.0) if TOL[dname] else all(
             np.array_equal(got[s], want[s]) for s in range(n1 + n2))
-        print(f"dist_check world={world} n1={n1} n2={n2} {dname} steps={steps} "
+        print(f"dist_check world={world} n1={n1} n2={n2} {dname} steps={steps} {launch} {policy} "
               f"worst_rel_err={worst:.3e} {'PASS' if ok else 'FAIL'}", flush=True)
     grp.close()
     dist.barrier()

@@ -32,6 +32,15 @@ def test_two_gpus_tp2_tp1():
     _run(2, 2, 1, "f32", 2)
 
 
+@pytest.mark.parametrize("launch,policy", [("three", "split"), ("alternate", "split"),
+                                           ("fused", "healthy"), ("alternate", "healthy")])
+def test_two_gpus_step_launch_variants(launch, policy):
+    """One launch per step (ntp_grad_sync_step) and the three-launch sequence
+    interoperate; with the "healthy" policy the degraded GPU computes nothing
+    and its step is the handshake-only kernel."""
+    _run(2, 4, 3, "f32", 4, launch, policy)
+
+
 def test_four_gpus_tp2_tp1():
     _run(4, 2, 1, "f32", 2)
 
