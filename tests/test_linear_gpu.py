@@ -112,6 +112,8 @@ def test_gemm_split_k_tail(Lin, M, N, K, a_mn, b_mn):
             Lin.mm(A, B, Y, epilogue="gelu", aux=H)
             D = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
             Lin.mm(A, B, D, epilogue="dgelu", aux=H)
+            want_d = acc.double().cpu().numpy() * O.gelu_grad(H.double().cpu().numpy())
+            assert rel(D.float().cpu(), torch.from_numpy(want_d)) < 5e-3
             # fused red epilogue: the local copy and a "partner" copy both get alpha*acc
             loc = torch.zeros((M, N), dtype=torch.float32, device="cuda")
             far = torch.zeros((M, N), dtype=torch.float32, device="cuda")
