@@ -440,18 +440,23 @@ class NtpDpMultiGroup:
         sp = ctypes.c_void_p(s.cuda_stream)
         st = ctypes.cast(self._status.data_ptr(), ctypes.POINTER(ctypes.c_int))
         n = len(self.partners)
+        none = _lib.u64_ptr_array([])
+
+        def exchange(kind):
+            # post this process's words and wait for the partners' in one launch
+            # (ntp_grad_sync_step with no plan runs only the handshakes)
+            _lib.check(L.ntp_grad_sync_step(
+                None, None, 0, OPS["weighted"], 1.0, 1.0,
+                _lib.u64_ptr_array(self._words(kind, False)), n,
+                _lib.u64_ptr_array(self._words(kind, True)), n, none, 0, none, 0,
+                e, int(spin_ns), st, sp), "ntp_grad_sync_step")
+
         if n:
-            _lib.check(L.ntp_signal_post(_lib.u64_ptr_array(self._words(READY, False)), n, e, sp),
-                       "ntp_signal_post")
-            _lib.check(L.ntp_signal_wait(_lib.u64_ptr_array(self._words(READY, True)), n, e,
-                                         spin_ns, st, sp), "ntp_signal_wait")
+            exchange(READY)
         if self.plan is not None:
             self.plan.sync(self.bufs, OPS["weighted"], self.w, s)
         if n:
-            _lib.check(L.ntp_signal_post(_lib.u64_ptr_array(self._words(DONE, False)), n, e, sp),
-                       "ntp_signal_post")
-            _lib.check(L.ntp_signal_wait(_lib.u64_ptr_array(self._words(DONE, True)), n, e,
-                                         spin_ns, st, sp), "ntp_signal_wait")
+            exchange(DONE)
 
     def status(self) -> int:
         return int(self._status.item()) if self._status is not None else 0
