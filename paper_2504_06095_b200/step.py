@@ -10,7 +10,9 @@ the best measured configuration (scripts/step_bench.py):
   * the TMA-bulk sync kernel on `sync_ctas` SMs and the persistent GEMMs on the
     rest, so neither waits for the other's CTAs to drain;
   * executor policy "healthy": the degraded GPU, which holds the most units,
-    only serves its arena and runs no sync kernel beside its GEMMs.
+    only serves its arena and runs no sync kernel beside its GEMMs;
+  * the first layer's sync, which no GEMM is left to hide, runs on every SM
+    (``uncap_last``).
 """
 
 from __future__ import annotations
@@ -26,8 +28,9 @@ class OverlappedBackward:
     arenas.  ``run(inputs)`` with inputs[l] = [(X, G), ...] per shard."""
 
     def __init__(self, layers, w_h: float, w_r: float, *, sync_ctas: int = 16,
-                 policy: str = "healthy", device: int | None = None):
+                 policy: str = "healthy", device: int | None = None, uncap_last: bool = True):
         self.layers = layers
+        self.uncap_last = bool(uncap_last)
         self.w_h, self.w_r = float(w_h), float(w_r)
         self.sync_ctas = int(sync_ctas)
         self.device = torch.cuda.current_device() if device is None else device
@@ -53,6 +56,8 @@ class OverlappedBackward:
                     for (sh, grads), (X, G) in zip(shards, inputs[li]):
                         sh.backward(X, G, grads)
                 self.side.wait_stream(main)
+                if li == 0 and self.uncap_last:
+                    L.ntp_set_option(1, 0)  # launched after the last GEMM: every SM
                 group.step(self.w_h, self.w_r, self.side)
             main.wait_stream(self.side)
         finally:
