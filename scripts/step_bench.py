@@ -198,7 +198,7 @@ class Config:
         return {"gemm_done_ms": [round(t0.elapsed_time(e), 3) for e in g_end],
                 "sync_done_ms": [round(t0.elapsed_time(e), 3) for e in s_end]}
 
-    def product(self, uncap_last=True):
+    def product(self, uncap_last=True, sync_ctas=16):
         """The package's OverlappedBackward over this configuration."""
         if getattr(self, "_ob", None) is None:
             from paper_2504_06095_b200.step import OverlappedBackward
@@ -208,6 +208,7 @@ class Config:
             self._ob_inputs = [[(X, G) for sh, X, G, grads in self.shards[li]]
                                for li in range(self.L)]
         self._ob.uncap_last = uncap_last
+        self._ob.sync_ctas = sync_ctas
         self._ob.run(self._ob_inputs, self.main)
 
     def set_policy(self, policy):
@@ -269,6 +270,9 @@ def modes(Lb, sms):
         # the same configuration through the package API (step.OverlappedBackward)
         "product_overlapped": (opts(), lambda c: c.product(), "healthy"),
         "product_overlapped_capped_last": (opts(), lambda c: c.product(False), "healthy"),
+        "product_overlapped_sync8": (opts(), lambda c: c.product(True, 8), "healthy"),
+        "product_overlapped_sync24": (opts(), lambda c: c.product(True, 24), "healthy"),
+        "product_overlapped_sync32": (opts(), lambda c: c.product(True, 32), "healthy"),
         "overlap_bulk_cap16_healthy_pdl": (opts(2, 16, sms - 16),
                                            lambda c: c.backward(True, pdl=True), "healthy"),
         "fused_red": (opts(), lambda c: c.fused_backward("red")),
