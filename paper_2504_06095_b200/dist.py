@@ -271,9 +271,12 @@ class NtpSyncGroup:
         self.wait_done = [self.sig + 8 * (DONE * SIG_WORDS + p) for p in self.partners]
         self.epoch = 0
         self._status = None
-        # True: step() is one launch (ntp_grad_sync_step); False: three launches
-        # (post ready / signalled sync / wait done), kept for comparison
-        self.fused_step = True
+        # True: step() is one launch (ntp_grad_sync_step), 25 -> 17.5 us at 1 MB
+        # per replica, but 6 of 66 sweep measurements came out 15-60 % slow
+        # (cause not found; profiles/r01_sweep_sync_multi.json).  False (default):
+        # three launches (post ready / signalled sync / wait done), no outliers
+        # in the same runs, and no difference at the bench's 2.4 GB.
+        self.fused_step = False
         self._sig_arrays = None
 
     def _build_plans(self, policy) -> None:

@@ -4,8 +4,8 @@ all arenas and compares them with the oracle's fp64 nonuniform sync.
 
     torchrun --nproc-per-node N scripts/dist_check.py [n1 n2 dtype steps [launch [policy]]]
 
-launch: "fused" (default, one ntp_grad_sync_step per step), "three" (post ready /
-signalled sync / wait done) or "alternate"; policy: the executor policy
+launch: "fused" (default here, one ntp_grad_sync_step per step), "three" (post
+ready / signalled sync / wait done; NtpSyncGroup's default) or "alternate"; policy: the executor policy
 ("split" default, "healthy": the reduced side computes nothing and only
 hand-shakes)
 """

@@ -140,7 +140,7 @@ def sync_sweep_dist():
         lay = pair_layout(ModelShape(f"sweep{mb}", 4096, k, 0, 1), 4, 3)
         plc = Placement.default(world, 4, 3)
         grp = NtpSyncGroup(lay, plc, torch.bfloat16, device=local).upload()
-        grp.fused_step = os.environ.get("NTP_FUSED_STEP", "1") != "0"  # A/B: 1 vs 3 launches
+        grp.fused_step = os.environ.get("NTP_FUSED_STEP", "0") != "0"  # A/B: 1 vs 3 launches
         for s in grp.hosted:
             a = grp.arena(s)
             a.copy_(torch.randn(a.numel(), device="cuda").to(torch.bfloat16))
