@@ -278,6 +278,7 @@ class NtpSyncGroup:
         # in the same runs, and no difference at the bench's 2.4 GB.
         self.fused_step = False
         self._sig_arrays = None
+        self._bufs_array = None
 
     def _build_plans(self, policy) -> None:
         """What this process computes under an executor policy, which peer
@@ -292,6 +293,7 @@ class NtpSyncGroup:
         order = sorted(self.slot_ptr)
         self.buf_index = {s: i for i, s in enumerate(order)}
         self.bufs = [self.slot_ptr[s] for s in order]
+        self._bufs_array = None
         remap = np.full(placement.n1 + placement.n2, -1, dtype=np.int64)
         for s, i in self.buf_index.items():
             remap[s] = i
@@ -366,14 +368,16 @@ class NtpSyncGroup:
         s = torch.cuda.current_stream(self.device) if stream is None else stream
         sp = ctypes.c_void_p(s.cuda_stream)
         st = ctypes.cast(self._status.data_ptr(), ctypes.POINTER(ctypes.c_int))
+        if self._sig_arrays is None:  # ctypes arrays built once (host cost per step)
+            self._sig_arrays = tuple(_lib.u64_ptr_array(w) for w in
+                                     (self.post_ready, self.wait_ready, self.post_done,
+                                      self.wait_done))
+        pr, wr, pd, wd = self._sig_arrays
+        if self._bufs_array is None:
+            self._bufs_array = _lib.ptr_array(self.bufs)
+        bufs = self._bufs_array
         if self.fused_step and self.partners:
             # one launch: post ready, wait ready, sync, post done, wait done
-            if self._sig_arrays is None:
-                self._sig_arrays = tuple(_lib.u64_ptr_array(w) for w in
-                                         (self.post_ready, self.wait_ready, self.post_done,
-                                          self.wait_done))
-            pr, wr, pd, wd = self._sig_arrays
-            bufs = _lib.ptr_array(self.bufs)
             _lib.check(L.ntp_grad_sync_step(
                 plan._h if plan is not None else None, bufs, len(self.bufs), OPS["weighted"],
                 float(w_h), float(w_r), pr, len(self.post_ready), wr, len(self.wait_ready),
@@ -381,24 +385,23 @@ class NtpSyncGroup:
                 "ntp_grad_sync_step")
             return
         if self.post_ready:
-            _lib.check(L.ntp_signal_post(_lib.u64_ptr_array(self.post_ready), len(self.post_ready),
-                                         e, sp), "ntp_signal_post")
+            _lib.check(L.ntp_signal_post(pr, len(self.post_ready), e, sp), "ntp_signal_post")
         if plan is not None:
             if self.partners:
-                plan.grad_sync_signaled(self.bufs, OPS["weighted"], w_h, w_r,
-                                        self.wait_ready, self.post_done, e, spin_ns,
-                                        self._status.data_ptr(), s)
+                _lib.check(L.ntp_grad_sync_signaled(
+                    plan._h, bufs, len(self.bufs), OPS["weighted"], float(w_h), float(w_r),
+                    wr, len(self.wait_ready), pd, len(self.post_done), e, int(spin_ns), st, sp),
+                    "ntp_grad_sync_signaled")
             else:
                 plan.grad_sync(self.bufs, OPS["weighted"], w_h, w_r, s)
         elif self.partners:
             # nothing to compute: wait until partners may be touched, then release them
-            _lib.check(L.ntp_signal_wait(_lib.u64_ptr_array(self.wait_ready), len(self.wait_ready),
-                                         e, spin_ns, st, sp), "ntp_signal_wait")
-            _lib.check(L.ntp_signal_post(_lib.u64_ptr_array(self.post_done), len(self.post_done),
-                                         e, sp), "ntp_signal_post")
+            _lib.check(L.ntp_signal_wait(wr, len(self.wait_ready), e, spin_ns, st, sp),
+                       "ntp_signal_wait")
+            _lib.check(L.ntp_signal_post(pd, len(self.post_done), e, sp), "ntp_signal_post")
         if self.wait_done:
-            _lib.check(L.ntp_signal_wait(_lib.u64_ptr_array(self.wait_done), len(self.wait_done),
-                                         e, spin_ns, st, sp), "ntp_signal_wait")
+            _lib.check(L.ntp_signal_wait(wd, len(self.wait_done), e, spin_ns, st, sp),
+                       "ntp_signal_wait")
 
     def open_slots(self, slots) -> list:
         """Device pointers of the given logical slots (IPC-mapping peers' arenas
