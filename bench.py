@@ -38,6 +38,40 @@ sys.path.insert(0, ROOT)
 
 METRIC = "NTP grad-sync GB/s & % NVLink roofline (device-timed, max over ranks) vs CPU ref"
 W_H, W_R = 4.0 / 7.0, 3.0 / 7.0  # local-batch share of TP4 (lb 4) and TP3 (lb 3) replicas
+L2_BYTES = 126 << 20
+
+# BASELINE.json configs, restated here so the reference arm needs no product
+# import (tests/test_bench_contract.py checks they equal workloads.SHAPES)
+WORKLOADS = {
+    # name: (hidden, ffn, heads, layers, dtype, BASELINE.json config)
+    "gpt-1.3b": (2048, 8192, 16, 24, "bf16", "configs[1]"),
+    "llama3-8b-shaped": (4096, 14336, 32, 32, "bf16", "configs[3]"),
+    "mlp-h1024-ffn4096": (1024, 4096, 0, 1, "f32", "configs[0]"),
+}
+ELEM_BYTES = {"bf16": 2, "f32": 4}
+
+
+def workload_elems(name: str) -> int:
+    """Elements of one replica's gradient (every layer, MLP + attention units)."""
+    hidden, ffn, heads, layers = WORKLOADS[name][:4]
+    per = ffn * 2 * hidden + (heads * 4 * hidden * (hidden // heads) if heads else 0)
+    return layers * per
+
+
+def workload_config(name: str, n_gpus: int) -> dict:
+    """The `config` object both arms print (identical, so the driver can pair them)."""
+    hidden, ffn, heads, layers, dt, which = WORKLOADS[name]
+    S = workload_elems(name)
+    eb = ELEM_BYTES[dt]
+    l2 = ("inputs %.1f GB >> 126 MB L2 (no flush needed)" % (2 * S * eb / 1e9)
+          if 2 * S * eb > 2 * L2_BYTES else
+          "inputs %.0f MB < 2x L2: L2 flushed (256 MB write) before every timed step"
+          % (2 * S * eb / 1e6))
+    return {"workload": f"{name} DP=2 TP4+TP3 full-step grad sync (BASELINE {which}), "
+                        f"{'7 logical ranks on 1 GPU' if n_gpus == 1 else 'logical ranks over %d GPUs' % n_gpus}",
+            "layers": layers, "hidden": hidden, "ffn": ffn, "heads": heads,
+            "grad_bytes_per_replica": S * eb, "weights": [round(W_H, 6), round(W_R, 6)],
+            "l2": l2}
 
 
 def peaks():
@@ -114,47 +148,101 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+class NvlinkCounters:
+    """NVLink data bytes this GPU sent / received during the timed region, from
+    NVML's per-link throughput counters (NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX /
+    _RX, KiB, summed over the links that report; scripts/nvml_nvlink_probe.py
+    checks them against a known peer copy).  None when NVML cannot read them."""
+
+    TX, RX, LINKS = 138, 139, 18
+
+    def __init__(self, device_index: int):
+        self.h = None
+        self.src = "unavailable"
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(device_index)
+        except Exception as e:  # noqa: BLE001 (NVML missing or no permission: report None)
+            self.src = f"unavailable: {e}"
+
+    def _read(self):
+        if self.h is None:
+            return None
+        ids = [(f, link) for f in (self.TX, self.RX) for link in range(self.LINKS)]
+        try:
+            vals = self.N.nvmlDeviceGetFieldValues(self.h, ids)
+        except Exception as e:  # noqa: BLE001
+            self.src = f"unavailable: {e}"
+            return None
+        tx = rx = 0
+        ok = 0
+        for (f, _), v in zip(ids, vals):
+            if v.nvmlReturn != 0:
+                continue
+            ok += 1
+            if f == self.TX:
+                tx += int(v.value.ullVal)
+            else:
+                rx += int(v.value.ullVal)
+        if not ok:
+            self.src = "unavailable: no NVLink throughput field readable"
+            return None
+        self.src = f"NVML fields 138/139 (KiB) over {ok // 2} links"
+        return tx * 1024, rx * 1024
+
+    def start(self):
+        self.t0 = self._read()
+
+    def stop(self):
+        t1 = self._read()
+        if self.t0 is None or t1 is None:
+            return {"tx_bytes": None, "rx_bytes": None, "src": self.src}
+        return {"tx_bytes": t1[0] - self.t0[0], "rx_bytes": t1[1] - self.t0[1], "src": self.src}
+
+
 # ---------------------------------------------------------------------------
 # CPU baseline: the oracle restatement of the reference's nonuniform_grad_sync
 
 
-def cpu_sample(shape, n1, n2, layers=1, threads=None, reps=3, seed=0, passes=1):
+def cpu_sample(name, n1=4, n2=3, layers=1, threads=None, reps=3, seed=0, passes=1):
     """Time oracle.nonuniform_sync (fp64, the reference's arithmetic) on `layers`
-    layers of the workload, `passes` times over the same host buffers (so a
-    whole multi-layer step can be timed with one layer's memory); returns
-    (seconds per pass set, best of reps; elements per pass; threads)."""
+    layers of workload `name`, `passes` times over the same host buffers (so a
+    whole multi-layer step is timed with one layer's memory: every layer has
+    the same shard maps and sizes); returns (seconds for one pass set, best of
+    reps; elements per pass; threads).  Only oracle/ is used: no product code
+    runs or loads on this leg."""
     from oracle import oracle as O
-    from paper_2504_06095_b200.workloads import pair_layout
     if threads:
         O.set_threads(threads)
-    lay = pair_layout(shape, n1, n2, layers=layers)
+    hidden, ffn, heads = WORKLOADS[name][:3]
+    segs, h_elems, r_elems = O.pair_layout(hidden, ffn, heads, layers, n1, n2)
     rng = np.random.default_rng(seed)
     best = float("inf")
-    hb = [rng.standard_normal(e) for e in lay.h_elems]
-    rb = [rng.standard_normal(e) for e in lay.r_elems]
+    hb = [rng.standard_normal(e) for e in h_elems]
+    rb = [rng.standard_normal(e) for e in r_elems]
+    # per-segment contiguous views into the rank arenas (unit-major)
+    views = [O.segment_views(seg, hb, rb) for seg in segs]
     for _ in range(reps):
         t = 0.0
-        for k, unit, hc, rc, h_base, r_base in lay.segs:
-            # per-segment views into the rank arenas (unit-major)
-            hv = [np.ascontiguousarray(b[s:s + len(c) * unit]) for b, c, s in zip(hb, hc, h_base)]
-            rv = [np.ascontiguousarray(b[s:s + len(c) * unit]) for b, c, s in zip(rb, rc, r_base)]
-            smap_comp = np.empty(k, dtype=np.int64)
-            smap_sync = np.empty(k, dtype=np.int64)
-            for r, c in enumerate(hc):
-                smap_comp[c] = r
-            for r, c in enumerate(rc):
-                smap_sync[c] = r
-            for _ in range(passes):
-                t0 = time.perf_counter()
-                O.nonuniform_sync(smap_comp, smap_sync, hc, rc, hv, rv, unit, op=O.OP_WEIGHTED,
-                                  weights=(W_H, W_R))
-                t += time.perf_counter() - t0
+        for _ in range(passes):
+            t0 = time.perf_counter()
+            for seg, (hv, rv) in zip(segs, views):
+                O.nonuniform_sync(seg[2], seg[3], seg[4], seg[5], hv, rv, seg[1],
+                                  op=O.OP_WEIGHTED, weights=(W_H, W_R))
+            t += time.perf_counter() - t0
         best = min(best, t)
-    return best, lay.elems, O.num_threads()
+    return best, sum(h_elems), O.num_threads()
 
 
 # ---------------------------------------------------------------------------
 # our arm, one GPU
+
+
+def _torch_dtype(name):
+    import torch
+    return {"bf16": torch.bfloat16, "f32": torch.float32}[WORKLOADS[name][4]]
 
 
 def run_single(args):
@@ -167,8 +255,8 @@ def run_single(args):
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     shape = SHAPES[args.workload]
-    dtype = torch.bfloat16
-    eb = 2
+    dtype = _torch_dtype(args.workload)
+    eb = ELEM_BYTES[WORKLOADS[args.workload][4]]
     lay = pair_layout(shape, 4, 3)
     plan = build_plan(lay, dtype).upload(0)
     gen = torch.Generator(device=dev).manual_seed(0)
@@ -177,6 +265,9 @@ def run_single(args):
     ptrs = tensor_ptrs(arenas)
     S = lay.elems
     stream = torch.cuda.current_stream(dev)
+    flush = None
+    if 2 * S * eb <= 2 * L2_BYTES:  # inputs could stay L2-resident: flush before each step
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def step():
         plan.grad_sync(ptrs, OPS["weighted"], W_H, W_R, stream)
@@ -186,51 +277,114 @@ def run_single(args):
     torch.cuda.synchronize()
     clocks = ClockSampler(dev.index)
     clocks.start()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * (args.steps if flush is not None else 1))]
     torch.cuda.synchronize()
     clocks.mark("t0")
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
+    if flush is None:
+        ev[0].record(stream)
+        for _ in range(args.steps):
+            step()
+        ev[1].record(stream)
+    else:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            ev[2 * i].record(stream)
+            step()
+            ev[2 * i + 1].record(stream)
     torch.cuda.synchronize()
     clocks.mark("t1")
-    ms_total = e0.elapsed_time(e1)
+    ms_total = sum(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(len(ev) // 2))
     clk = clocks.stop()
     ms = ms_total / args.steps
     value = S * eb / (ms * 1e-3) / 1e9
     pk = peaks()
     hbm_bytes = 4 * S * eb  # read both replicas, write both
     achieved = hbm_bytes / (ms * 1e-3) / 1e9
-    roof = {"bound": "hbm", "kernel": "ntp::plan_kernel_bulk<bf16,weighted,4>",
+    kname = "ntp::plan_kernel_%s<%s,weighted>" % (
+        "bulk" if plan.stats["n_chunks"] >= 4 * 148 else "vec", WORKLOADS[args.workload][4])
+    roof = {"bound": "hbm", "kernel": kname,
             "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "peak_src": pk["src"],
             "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
-            "algorithmic_bytes_per_launch": hbm_bytes, "traffic": _ncu_traffic()}
+            "algorithmic_bytes_per_launch": hbm_bytes,
+            "traffic": _ncu_traffic(args.workload)}
     out = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": 1,
            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4),
-           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-           "data": "synthetic (N(0,1) bf16 gradients, torch.Generator seed 0)",
-           "config": {"workload": f"{shape.name} DP=2 TP4+TP3 full-step grad sync "
-                                  "(BASELINE configs[1]), 7 logical ranks on 1 GPU",
-                      "layers": shape.layers, "hidden": shape.hidden, "ffn": shape.ffn,
-                      "heads": shape.heads, "grad_bytes_per_replica": S * eb,
-                      "weights": [round(W_H, 6), round(W_R, 6)],
-                      "l2": "inputs 4.8 GB >> 126 MB L2 (no flush needed)",
-                      "plan_chunks": plan.stats["n_chunks"]},
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+           "dtype": WORKLOADS[args.workload][4],
+           "data": "synthetic (N(0,1) gradients, torch.Generator seed 0)",
+           "config": workload_config(args.workload, 1),
+           "plan": {"chunks": plan.stats["n_chunks"], "table_bytes": 16 * plan.stats["n_chunks"]},
            "roofline": roof, "gpu_launches": args.steps, "clocks": clk}
+    if args.check:
+        out["check"] = check_single(args, lay, plan, arenas, dtype)
     if not args.no_e2e:
         out["e2e"] = run_e2e_single(args, lay, plan, dtype, eb)
     if not args.no_cpu:
         # one whole step of the workload: all layers synced in turn through one
-        # layer's host buffers (memory stays at one layer), best of 8 (~10 s)
-        t, elems, thr = cpu_sample(shape, 4, 3, layers=1, passes=shape.layers, reps=8)
+        # layer's host buffers (memory stays at one layer), best of a few (~10 s)
+        reps = 8 if shape.layers > 1 else 40
+        t, elems, thr = cpu_sample(args.workload, 4, 3, layers=1, passes=shape.layers, reps=reps)
         out["cpu_baseline"] = {"value": round(shape.layers * elems * eb / t / 1e9, 3),
                                "unit": "GB/s", "cores": thr, "kind": "port",
-                               "sample": f"one full step: {shape.layers} layers x {elems} elements "
+                               "sample": f"one full step: {shape.layers} layer(s) x {elems} elements "
                                          "per replica, each layer through the same host buffers; "
-                                         "oracle fp64 3-step nonuniform_grad_sync, best of 8 steps",
-                               "seconds_per_step": round(t, 3)}
+                                         "oracle fp64 3-step nonuniform_grad_sync, "
+                                         f"best of {reps} steps",
+                               "seconds_per_step": round(t, 4)}
     return out
+
+
+def check_single(args, lay, plan, arenas, dtype):
+    """--check: one more step on fresh inputs, every segment of every layer
+    against the fp64 oracle."""
+    hidden, ffn, heads, layers = WORKLOADS[args.workload][:4]
+    return check_pair_arenas(hidden, ffn, heads, layers, plan, arenas, dtype, lay.h_elems,
+                             lay.r_elems)
+
+
+def check_pair_arenas(hidden, ffn, heads, layers, plan, arenas, dtype, h_elems, r_elems,
+                      seed=12345, weights=(W_H, W_R), n1=4, n2=3):
+    """Fill the 1-GPU arenas with fresh N(0,1) values, run ONE sync through
+    `plan`, then compare every segment of every layer with the fp64 oracle on
+    the same dtype-rounded inputs (streamed segment by segment).  The layout
+    used to slice the arenas comes from the oracle's own shard map, and must
+    equal the product's.  Returns a summary; raises when a segment is off."""
+    import torch
+    from oracle import oracle as O
+    from paper_2504_06095_b200.plans import OPS, tensor_ptrs
+    segs, oh, orr = O.pair_layout(hidden, ffn, heads, layers, n1, n2)
+    if oh != list(h_elems) or orr != list(r_elems):
+        raise RuntimeError("product arena layout differs from the oracle's")
+    gen = torch.Generator(device=arenas[0].device).manual_seed(seed)
+    for a in arenas:
+        a.copy_(torch.randn(a.numel(), generator=gen, device=a.device).to(dtype))
+    before = [a.cpu() for a in arenas]
+    plan.grad_sync(tensor_ptrs(arenas), OPS["weighted"], weights[0], weights[1])
+    torch.cuda.synchronize()
+    after = [a.cpu() for a in arenas]
+    worst, identical, t0 = 0.0, True, time.perf_counter()
+    tol = {torch.bfloat16: 2e-2, torch.float16: 2e-3, torch.float32: 1e-6}[dtype]
+    errs = []
+
+    def f64(views):
+        return [v.double().numpy() for v in views]
+    for seg in segs:
+        hv_in, rv_in = O.segment_views(seg, before[:n1], before[n1:])
+        hv_out, rv_out = O.segment_views(seg, after[:n1], after[n1:])
+        err, same = O.check_pair_segment(seg, f64(hv_in), f64(rv_in), f64(hv_out), f64(rv_out),
+                                         weights)
+        errs.append(err)
+        worst = max(worst, err)
+        identical &= same
+    ok = worst <= tol and identical
+    res = {"ok": ok, "segments": len(segs), "max_rel_err": worst, "tol": tol,
+           "replicas_bit_identical": identical, "chunks": plan.stats["n_chunks"],
+           "seconds": round(time.perf_counter() - t0, 1),
+           "oracle": "oracle.nonuniform_sync fp64 (tpnumerics.py:289-356) on the same rounded inputs"}
+    if not ok:
+        bad = [i for i, e in enumerate(errs) if e > tol]
+        raise RuntimeError(f"parity check failed: {res}, segments over tol: {bad[:10]}")
+    return res
 
 
 def run_e2e_single(args, lay, plan, dtype, eb):
@@ -243,7 +397,8 @@ def run_e2e_single(args, lay, plan, dtype, eb):
     spp = int(os.environ.get("NTP_E2E_SEGS_PER_PIECE", "0")) or None
     hs = HostSync(plan, [e for e in lay.h_elems + lay.r_elems], dtype, device=0,
                   piece_plans=layer_pieces(lay, dtype, 0, layers_per_piece=lpp,
-                                           segs_per_piece=spp))
+                                           segs_per_piece=spp),
+                  back_to_back=True)  # the timed loop re-runs the same host buffers
     gen = torch.Generator().manual_seed(1)
     host = [torch.randn(e, generator=gen, dtype=torch.float32).to(dtype).pin_memory()
             for e in lay.h_elems + lay.r_elems]
@@ -308,11 +463,16 @@ def run_e2e_single(args, lay, plan, dtype, eb):
             "host_link_frac": round(nbytes / (duplex_gbs * 1e9) * 1e3 / ms, 3)}
 
 
-def _ncu_traffic():
+def _ncu_traffic(workload):
+    """DRAM bytes per launch of the bench kernel from the committed ncu --set
+    full capture (profiles/ncu_traffic.json, keyed by workload)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(path):
         with open(path) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            d = json.load(f)
+        rec = d.get(workload)
+        if rec:
+            return rec.get("dram_bytes_per_launch")
     return None
 
 
@@ -321,31 +481,55 @@ def _ncu_traffic():
 
 
 def run_reference(args):
-    from paper_2504_06095_b200.workloads import SHAPES
+    """The reference's CPU path (the oracle's C restatement of
+    tpnumerics.py:289-356, fp64, every host thread) on the SAME workload and
+    config as our arm: each timed step syncs every layer of the workload.  Only
+    oracle/ runs here (the product library is never imported or loaded)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
-    shape = SHAPES[args.workload]
-    eb = 2
+    name = args.workload
+    layers = WORKLOADS[name][3]
+    eb = ELEM_BYTES[WORKLOADS[name][4]]
     times = []
+    thr = 0
+    elems = 0
     for i in range(max(args.warmup, 0) + args.steps):
-        t, elems, thr = cpu_sample(shape, 4, 3, layers=1, reps=1, seed=i)
+        t, elems, thr = cpu_sample(name, 4, 3, layers=1, passes=layers, reps=1, seed=i)
         if i >= args.warmup:
             times.append(t)
     ms = 1e3 * float(np.mean(times))
-    value = elems * eb / (ms * 1e-3) / 1e9
+    S = layers * elems
+    assert S == workload_elems(name)
+    value = S * eb / (ms * 1e-3) / 1e9
+    sample = (f"every step = the whole workload: {layers} layer(s) x {elems} elements per "
+              "replica, synced layer by layer through one layer's host buffers (same shard maps "
+              "and sizes as every layer); oracle/ntp_oracle.c fp64 restatement of "
+              "tpnumerics.py:289-356 (the reference is pure Python; its 405 ms C1 time is in "
+              "BASELINE.md)")
     return {"metric": METRIC, "impl": "reference", "value": round(value, 3), "unit": "GB/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (N(0,1))",
-            "config": {"workload": f"{shape.name} DP=2 TP4+TP3 grad sync, 1-layer sample per step"},
+            "config": workload_config(name, args.gpus),
             "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": thr, "kind": "port",
-                             "sample": f"1 of {shape.layers} layers ({elems} elements per replica) "
-                                       "per step; oracle/ntp_oracle.c restatement of "
-                                       "tpnumerics.py:289-356 (the reference is pure Python; "
-                                       "its 405 ms C1 time is in BASELINE.md)"},
+                             "sample": sample},
             "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+
+
+def _reexec_torchrun(args, argv):
+    """`python bench.py --gpus N` (N>1) outside torchrun: relaunch this script
+    under torch.distributed.run with one process per GPU (127.0.0.1 rendezvous)."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + list(argv)
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
 
 
 def main(argv=None):
@@ -358,12 +542,19 @@ def main(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--check", action="store_true",
+                    help="after the timed region, check every segment of one more step "
+                         "against the fp64 oracle (N=1)")
     args = ap.parse_args(argv)
+    if args.workload not in WORKLOADS:
+        ap.error(f"--workload must be one of {sorted(WORKLOADS)}")
     if args.impl == "reference":
         out = run_reference(args)
         if out is not None:
             print(json.dumps(out), flush=True)
         return 0
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _reexec_torchrun(args, sys.argv[1:] if argv is None else argv)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     with _stdout_to_stderr():  # library banners (NCCL's version line) stay off stdout
         if world > 1 or args.gpus > 1:

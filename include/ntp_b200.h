@@ -272,6 +272,8 @@ int ntp_gemm_set_pair(int mode);
  * to c CTAs (NTP_OPT_SYNC_MAX_CTAS), a GEMM cap of SMs - c lets the two run
  * side by side when the sync overlaps the backward pass. */
 int ntp_gemm_set_max_ctas(int n);
+/* The current cap (so a caller that changes it can restore it). */
+int ntp_gemm_get_max_ctas(void);
 
 /* 1 (default): when the persistent schedule ends in a partial wave of R tiles,
  * those tiles are split along K into up to 8 pieces run by idle CTA pairs; fp32

@@ -91,6 +91,7 @@ SIGNATURES = {
                                          ctypes.c_int64, ctypes.c_int, _vp]),
     "ntp_gemm_set_pair": (ctypes.c_int, [ctypes.c_int]),
     "ntp_gemm_set_max_ctas": (ctypes.c_int, [ctypes.c_int]),
+    "ntp_gemm_get_max_ctas": (ctypes.c_int, []),
     "ntp_gemm_set_split_k": (ctypes.c_int, [ctypes.c_int]),
     "ntp_gemm_set_pdl": (ctypes.c_int, [ctypes.c_int]),
     "ntp_alloc": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, _vpp]),

@@ -1309,6 +1309,8 @@ extern "C" int ntp_gemm_set_max_ctas(int n) {
   return NTP_OK;
 }
 
+extern "C" int ntp_gemm_get_max_ctas(void) { return gemm::g_max_ctas.load(); }
+
 // 1 (default): CTA-pair tiles (tcgen05 cta_group::2), width picked per shape;
 // 0: 1-SM tiles; 2 / 3: force 256x128 / 256x256 pair tiles.
 extern "C" int ntp_gemm_set_pair(int mode) {

@@ -218,13 +218,38 @@ __device__ __forceinline__ void post_signals(uint64_t *const *post, int n, uint6
   for (int i = 0; i < n; ++i) st_release_sys(post[i], epoch);
 }
 
-// Last CTA of a signalled launch: every CTA's stores are fenced -- post the
-// done words, then (single-launch step) wait for the partners' done words.
+// The plan's 256-byte counter block: u32 word 0 counts finished CTAs of the
+// current launch, u64 word 1 records the last epoch whose ready words were
+// posted, u32 word 4 counts CTAs of the current launch that timed out.
+__device__ __forceinline__ unsigned int *failed_ctas(const SignalArgs &sig) { return sig.counter + 4; }
+
+// Last CTA of a signalled launch: every CTA's stores are fenced -- reset the
+// block for the next launch, then post the done words and (single-launch
+// step) wait for the partners' done words.  If any CTA of this launch timed
+// out (it skipped its chunks) the done words are NOT posted: the partners
+// then time out too instead of consuming a partly reduced result, and every
+// process's status reports the failure.
 __device__ __forceinline__ void last_cta_finish(const SignalArgs &sig) {
   __threadfence_system();
+  const unsigned int failed = atomicExch(failed_ctas(sig), 0u);
   *sig.counter = 0u;
+  if (failed) return;
   for (int i = 0; i < sig.n_post; ++i) st_release_sys(sig.post[i], sig.epoch);
   if (sig.n_fin) wait_signals(sig.fin, sig.n_fin, sig.epoch, sig.spin_ns, sig.status);
+}
+
+// A CTA whose ready-wait timed out does no work but still counts itself, so
+// the counter block is reset by whichever CTA finishes last.
+template <bool kSignaled>
+__device__ __forceinline__ void cta_abort(const SignalArgs &sig) {
+  if constexpr (kSignaled) {
+    if (threadIdx.x == 0) {
+      atomicAdd(failed_ctas(sig), 1u);
+      __threadfence();
+      const unsigned int done = atomicAdd(sig.counter, 1u);
+      if (done == gridDim.x - 1) last_cta_finish(sig);
+    }
+  }
 }
 
 template <bool kSignaled>
@@ -265,7 +290,10 @@ template <typename T, int OP, bool kSignaled>
 __global__ void __launch_bounds__(kThreads)
 plan_kernel_vec(const Chunk *__restrict__ chunks, int n_chunks, BufTable bufs,
                 typename Acc<T>::type wa, typename Acc<T>::type wb, SignalArgs sig) {
-  if (!cta_prologue<kSignaled>(sig)) return;
+  if (!cta_prologue<kSignaled>(sig)) {
+    cta_abort<kSignaled>(sig);
+    return;
+  }
   const int tid = threadIdx.x;
   int c = blockIdx.x;
   uint4 rec = c < n_chunks ? __ldg(reinterpret_cast<const uint4 *>(chunks) + c) : make_uint4(0, 0, 0, 0);
@@ -379,7 +407,10 @@ plan_kernel_bulk(const Chunk *__restrict__ chunks, int n_chunks, BufTable bufs,
                  typename Acc<T>::type wa, typename Acc<T>::type wb, SignalArgs sig) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   auto &sm = *reinterpret_cast<BulkSmem<kStages> *>(smem_raw);
-  if (!cta_prologue<kSignaled>(sig)) return;
+  if (!cta_prologue<kSignaled>(sig)) {
+    cta_abort<kSignaled>(sig);
+    return;
+  }
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   if (tid == 0) {
@@ -461,7 +492,10 @@ template <typename T, int OP, bool kSignaled>
 __global__ void __launch_bounds__(kThreads)
 plan_kernel_scalar(const Chunk *__restrict__ chunks, int n_chunks, BufTable bufs,
                    typename Acc<T>::type wa, typename Acc<T>::type wb, SignalArgs sig) {
-  if (!cta_prologue<kSignaled>(sig)) return;
+  if (!cta_prologue<kSignaled>(sig)) {
+    cta_abort<kSignaled>(sig);
+    return;
+  }
   for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
     const uint4 rec = __ldg(reinterpret_cast<const uint4 *>(chunks) + c);
     T *a = reinterpret_cast<T *>(bufs.p[rec.w & 0xffffu]) + rec.x;
@@ -645,6 +679,15 @@ static int set_device(int device) {
   NTP_CUDA(cudaGetDevice(&cur));
   if (cur != device) NTP_CUDA(cudaSetDevice(device));
   return NTP_OK;
+}
+
+// Launches with no plan (handshake kernels) go to the stream's own device,
+// whatever the caller's current device is.
+static int set_device_of(cudaStream_t s) {
+  if (!s) return NTP_OK;  // legacy default stream: the current device's
+  int dev = -1;
+  NTP_CUDA(cudaStreamGetDevice(s, &dev));
+  return set_device(dev);
 }
 
 }  // namespace ntp
@@ -879,7 +922,7 @@ int ntp_grad_sync_step(const ntp_plan *p, void *const *bufs, int n_bufs, int op,
   sig.n_fin = n_wait_done;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (!p || p->chunks.empty()) {
-    if (p && (st = set_device(p->device))) return st;
+    if ((st = p ? set_device(p->device) : set_device_of(s))) return st;
     signal_step_kernel<<<1, 1, 0, s>>>(sig);
     NTP_CUDA(cudaGetLastError());
     return NTP_OK;
@@ -898,6 +941,7 @@ int ntp_signal_post(uint64_t *const *post, int n_post, uint64_t epoch, void *str
   SignalArgs sig;
   int st = fill_signals(sig, nullptr, 0, post, n_post, epoch, 0, nullptr);
   if (st) return st;
+  if ((st = set_device_of(static_cast<cudaStream_t>(stream)))) return st;
   signal_post_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(sig);
   NTP_CUDA(cudaGetLastError());
   return NTP_OK;
@@ -908,6 +952,7 @@ int ntp_signal_wait(uint64_t *const *wait, int n_wait, uint64_t epoch, uint64_t 
   SignalArgs sig;
   int st = fill_signals(sig, wait, n_wait, nullptr, 0, epoch, spin_ns, status);
   if (st) return st;
+  if ((st = set_device_of(static_cast<cudaStream_t>(stream)))) return st;
   signal_wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(sig);
   NTP_CUDA(cudaGetLastError());
   return NTP_OK;

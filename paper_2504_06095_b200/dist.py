@@ -46,6 +46,14 @@ from .workloads import PairLayout
 
 SIG_WORDS = 64             # per page: ready[64] then done[64] (uint64), slot = writer's world rank
 SIG_BYTES = 2 * SIG_WORDS * 8
+
+
+def check_signal_world(world: int) -> None:
+    """Signal slots are indexed by the writer's world rank inside a page of
+    SIG_WORDS ready words then SIG_WORDS done words: a larger world would
+    alias ready onto done words (or write past the page)."""
+    if world > SIG_WORDS:
+        raise ValueError(f"signal page holds {SIG_WORDS} ranks, world size is {world}")
 READY, DONE = 0, 1
 
 
@@ -239,6 +247,7 @@ class NtpSyncGroup:
         self.lay, self.plc, self.dtype, self.policy = lay, placement, dtype, policy
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        check_signal_world(self.world)
         self.device = device
         self.ops = ops if ops is not None else DeviceOps(device)
         self.eb = torch.empty(0, dtype=dtype).element_size()

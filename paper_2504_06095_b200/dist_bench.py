@@ -28,7 +28,8 @@ def _max(x: float) -> float:
 
 
 def run(args):
-    from bench import METRIC, W_H, W_R, ClockSampler, peaks  # noqa: I001 (repo root on sys.path)
+    from bench import (ELEM_BYTES, L2_BYTES, METRIC, W_H, W_R, WORKLOADS,  # noqa: I001 (repo root)
+                       ClockSampler, NvlinkCounters, peaks, workload_config)
 
     # NCCL warnings (and its version banner) go to stderr: bench.py keeps fd 1
     # pointed at stderr while this runs, so stdout is the one JSON line
@@ -45,7 +46,8 @@ def run(args):
     n1, n2 = 4, 3
     lay = pair_layout(shape, n1, n2)
     plc = Placement.default(world, n1, n2)
-    dtype, eb = torch.bfloat16, 2
+    dt = WORKLOADS[args.workload][4]
+    dtype, eb = {"bf16": torch.bfloat16, "f32": torch.float32}[dt], ELEM_BYTES[dt]
     nseg = len(shape.segments())
     pieces = [list(range(i * nseg, (i + 1) * nseg)) for i in range(lay.layers)]  # e2e: per layer
     grp = NtpSyncGroup(lay, plc, dtype, device=local, pieces=pieces).upload()
@@ -62,21 +64,42 @@ def run(args):
     dist.barrier()
     if grp.status() != 0:
         raise RuntimeError(f"rank {rank}: signal timeout during warm-up")
+    # small workloads would stay L2-resident between steps: flush (256 MB
+    # write) before every timed step, and time the steps alone
+    hosted_bytes = sum(grp.slot_elems[s] for s in grp.hosted) * eb
+    flush = (torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+             if 2 * lay.elems * eb <= 2 * L2_BYTES else None)
     clocks = ClockSampler(local)
     clocks.start()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nv = NvlinkCounters(local)
+    nev = 2 * (args.steps if flush is not None else 1)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(nev)]
     torch.cuda.synchronize()
     dist.barrier()
     clocks.mark("t0")
-    e0.record(stream)
-    for _ in range(args.steps):
-        grp.step(W_H, W_R, stream)
-    e1.record(stream)
+    nv.start()
+    if flush is None:
+        ev[0].record(stream)
+        for _ in range(args.steps):
+            grp.step(W_H, W_R, stream)
+        ev[1].record(stream)
+    else:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            ev[2 * i].record(stream)
+            grp.step(W_H, W_R, stream)
+            ev[2 * i + 1].record(stream)
     torch.cuda.synchronize()
+    nvl = nv.stop()
     clocks.mark("t1")
     dist.barrier()
     clk = clocks.stop()
-    ms = _max(e0.elapsed_time(e1) / args.steps)
+    ms = _max(sum(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(nev // 2)) / args.steps)
+    # NVLink bytes per step, per direction, busiest rank (NVML counters read
+    # around the timed region)
+    tx = _max(float(nvl["tx_bytes"]) / args.steps if nvl["tx_bytes"] is not None else -1.0)
+    rx = _max(float(nvl["rx_bytes"]) / args.steps if nvl["rx_bytes"] is not None else -1.0)
+    traffic = None if min(tx, rx) < 0 else int(max(tx, rx))
     kernel_ms = ms
     if grp.status() != 0:
         raise RuntimeError(f"rank {rank}: signal timeout")
@@ -90,20 +113,23 @@ def run(args):
         out = {"metric": METRIC, "value": round(S * eb / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
                "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
                "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
-               "vs_baseline": None, "dtype": "bf16",
-               "data": "synthetic (N(0,1) bf16 gradients)",
-               "config": {"workload": f"{shape.name} DP=2 TP4+TP3 full-step grad sync over NVLink",
-                          "placement_healthy": list(plc.h_proc),
-                          "placement_reduced": list(plc.r_proc),
-                          "grad_bytes_per_replica": S * eb,
-                          "busiest_gpu_bytes_per_direction": B,
-                          "weights": [round(W_H, 6), round(W_R, 6)],
-                          "l2": "inputs >> L2"},
-               "roofline": {"bound": "nvlink", "kernel": "ntp::plan_kernel_bulk<bf16,weighted,4,signaled>",
+               "vs_baseline": None, "dtype": dt,
+               "data": "synthetic (N(0,1) gradients)",
+               "config": workload_config(args.workload, world),
+               "placement": {"healthy": list(plc.h_proc), "reduced": list(plc.r_proc),
+                             "busiest_gpu_bytes_per_direction": B,
+                             "hosted_bytes_rank0": hosted_bytes},
+               "roofline": {"bound": "nvlink",
+                            "kernel": f"ntp::plan_kernel_bulk<{dt},weighted,4,signaled>",
                             "achieved": round(achieved, 1), "peak": pk["nvlink_gbs"],
                             "peak_src": "measured peer copy 770 GB/s/direction (B200_PROFILING.md)",
                             "unit": "GB/s", "frac": round(achieved / pk["nvlink_gbs"], 4),
-                            "algorithmic_bytes_per_launch": B, "traffic": None,
+                            "algorithmic_bytes_per_launch": B, "traffic": traffic,
+                            "traffic_src": "NVML NVLink data counters around the timed region, "
+                                           "busiest rank, max(tx, rx) bytes per step "
+                                           f"({nvl['src']})",
+                            "traffic_over_algorithmic": (round(traffic / B, 3) if traffic and B
+                                                         else None),
                             "kernel_ms": round(kernel_ms, 4)},
                "gpu_launches": args.steps * _launches_per_step(grp),
                "clocks": clk, "e2e": e2e}

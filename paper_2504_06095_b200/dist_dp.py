@@ -39,7 +39,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
-from .dist import READY, DONE, SIG_BYTES, SIG_WORDS, DeviceOps, _wrap
+from .dist import READY, DONE, SIG_BYTES, SIG_WORDS, DeviceOps, _wrap, check_signal_world
 from .plans import OPS, Plan, dtype_code
 from .shardmap import build_shard_map
 
@@ -80,6 +80,7 @@ class NtpDpGroup:
         self.k, self.unit, self.m, self.plc, self.dtype = k, unit, m, plc, dtype
         self.device = device
         self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        check_signal_world(self.world)
         self.ops = ops if ops is not None else DeviceOps(device)
         self.eb = torch.empty(0, dtype=dtype).element_size()
         w = np.asarray(weights, dtype=np.float64)
@@ -360,6 +361,7 @@ class NtpDpMultiGroup:
         self.k, self.unit, self.m, self.plc, self.dtype = k, unit, m, plc, dtype
         self.device = device
         self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        check_signal_world(self.world)
         self.ops = ops if ops is not None else DeviceOps(device)
         self.eb = torch.empty(0, dtype=dtype).element_size()
         R = m + 1

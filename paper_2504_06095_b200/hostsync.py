@@ -18,11 +18,22 @@ from .plans import OPS, Plan, tensor_ptrs
 
 
 class HostSync:
-    def __init__(self, plan: Plan, arena_elems, dtype, device: int = 0, piece_plans=None):
+    def __init__(self, plan: Plan, arena_elems, dtype, device: int = 0, piece_plans=None,
+                 back_to_back: bool = False):
         """plan: a finalized plan over the arenas (buffer i = arena i).
         piece_plans: optional [(plan_i, arena_ranges_i)] splitting the work into
         pipelined pieces; arena_ranges_i = [(arena, lo, hi)] element ranges the
-        piece reads and writes."""
+        piece reads and writes.
+
+        back_to_back=False (default): every run() is fully ordered on the
+        current stream -- its host-to-device copies start after everything the
+        caller queued on that stream before the call, and the stream waits for
+        its device-to-host copies at the end.  back_to_back=True is for a loop
+        of runs over the same host buffers that nothing else touches in
+        between: piece i's host-to-device copy then waits only for the previous
+        run's device-to-host copy of piece i (not for the whole previous run),
+        so both host-link directions stay busy across runs; the current stream
+        still waits for each run's device-to-host copies before later work."""
         self.dev = torch.device("cuda", device)
         self.plan = plan if plan.device is not None else plan.upload(device)
         self.arenas = [torch.empty(e, dtype=dtype, device=self.dev) for e in arena_elems]
@@ -31,6 +42,7 @@ class HostSync:
         self.h2d = torch.cuda.Stream(self.dev)
         self.d2h = torch.cuda.Stream(self.dev)
         self.launches_per_run = 1 if not piece_plans else len(piece_plans)
+        self.back_to_back = bool(back_to_back)
         self._d2h_done = None  # per piece: the previous run's D2H of that piece
 
     def run(self, host, w_a: float, w_b: float) -> None:
@@ -44,14 +56,15 @@ class HostSync:
             for d, h in zip(self.arenas, host):
                 h.copy_(d, non_blocking=True)
             return
-        # Piece i's H2D waits only for the previous run's D2H of piece i (same
-        # host and device ranges), not for the whole previous run: back-to-back
-        # runs keep both PCIe directions busy across the run boundary.
-        if self._d2h_done is None:
+        # back_to_back: piece i's H2D waits only for the previous run's D2H of
+        # piece i (same host and device ranges), not for the whole previous
+        # run, so consecutive runs keep both PCIe directions busy.
+        chained = self.back_to_back and self._d2h_done is not None
+        if not chained:
             self.h2d.wait_stream(cur)
         done = []
         for i, (plan_i, ranges) in enumerate(self.pieces):
-            if self._d2h_done is not None:
+            if chained:
                 self.h2d.wait_event(self._d2h_done[i])
             with torch.cuda.stream(self.h2d):
                 for a, lo, hi in ranges:

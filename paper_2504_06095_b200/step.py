@@ -42,10 +42,14 @@ class OverlappedBackward:
 
     def run(self, inputs, stream=None) -> None:
         """One backward step (all layers, last first) with every layer's sync
-        overlapped; stream-ordered on `stream` (default: current)."""
+        overlapped; stream-ordered on `stream` (default: current).  The sync
+        kernel choice and the sync / GEMM CTA caps are library-wide options:
+        they are set for the duration of the call and restored to the
+        caller's values afterwards (not thread-safe against other threads
+        changing them meanwhile)."""
         L = _lib.load()
         main = torch.cuda.current_stream(self.device) if stream is None else stream
-        saved = (int(L.ntp_get_option(0)), int(L.ntp_get_option(1)))
+        saved = (int(L.ntp_get_option(0)), int(L.ntp_get_option(1)), int(L.ntp_gemm_get_max_ctas()))
         L.ntp_set_option(0, 2)                       # TMA-bulk sync kernel
         L.ntp_set_option(1, self.sync_ctas)          # on sync_ctas SMs ...
         L.ntp_gemm_set_max_ctas(self.sms - self.sync_ctas)  # ... GEMMs on the rest
@@ -63,4 +67,4 @@ class OverlappedBackward:
         finally:
             L.ntp_set_option(0, saved[0])
             L.ntp_set_option(1, saved[1])
-            L.ntp_gemm_set_max_ctas(0)
+            L.ntp_gemm_set_max_ctas(saved[2])

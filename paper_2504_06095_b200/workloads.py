@@ -53,7 +53,7 @@ class ModelShape:
 C1 = ModelShape("mlp-h1024-ffn4096", 1024, 4096, 0, 1)
 GPT_1_3B = ModelShape("gpt-1.3b", 2048, 8192, 16, 24)
 LLAMA3_8B = ModelShape("llama3-8b-shaped", 4096, 14336, 32, 32)
-SHAPES = {s.name: s for s in (GPT_1_3B, LLAMA3_8B)}
+SHAPES = {s.name: s for s in (GPT_1_3B, LLAMA3_8B, C1)}
 
 
 @dataclass

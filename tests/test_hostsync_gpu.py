@@ -13,7 +13,8 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-def test_back_to_back_runs_see_previous_results():
+@pytest.mark.parametrize("back_to_back", [False, True], ids=["ordered", "back_to_back"])
+def test_back_to_back_runs_see_previous_results(back_to_back):
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
     from paper_2504_06095_b200.hostsync import HostSync
@@ -23,7 +24,7 @@ def test_back_to_back_runs_see_previous_results():
     dt = torch.float32
     plan = build_plan(lay, dt)
     hs = HostSync(plan, list(lay.h_elems) + list(lay.r_elems), dt, device=0,
-                  piece_plans=layer_pieces(lay, dt, 0))
+                  piece_plans=layer_pieces(lay, dt, 0), back_to_back=back_to_back)
     rng = np.random.default_rng(3)
     init = [np.round(rng.standard_normal(e) * 64) / 64 for e in list(lay.h_elems) + list(lay.r_elems)]
     host = [torch.from_numpy(a).to(dt).pin_memory() for a in init]
@@ -49,3 +50,31 @@ def test_back_to_back_runs_see_previous_results():
             rb[r][rbase[r]:rbase[r] + len(c) * unit] = rv[r]
     for got, want in zip(host, hb + rb):
         assert np.array_equal(got.numpy().astype(np.float64), 4.0 * want)
+
+
+def test_ordered_run_sees_stream_ordered_host_writes():
+    """Default ordering: a non_blocking device->host copy the caller queues on
+    the current stream between two runs (refilling the pinned inputs) lands
+    before the second run's host->device copies read them."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2504_06095_b200.hostsync import HostSync
+    from paper_2504_06095_b200.workloads import ModelShape, build_plan, layer_pieces, pair_layout
+    shape = ModelShape("tiny", hidden=64, ffn=600, heads=4, layers=6)
+    lay = pair_layout(shape, 4, 3)
+    dt = torch.float32
+    elems = list(lay.h_elems) + list(lay.r_elems)
+    hs = HostSync(build_plan(lay, dt), elems, dt, device=0, piece_plans=layer_pieces(lay, dt, 0))
+    host = [torch.ones(e, dtype=dt).pin_memory() for e in elems]
+    hs.run(host, 1.0, 1.0)
+    # a slow device producer, then the refill of every host arena with 3.0
+    big = torch.randn(4096, 4096, device="cuda")
+    for _ in range(20):
+        big = big @ big * 1e-3
+    fill = [torch.full((e,), 3.0, dtype=dt, device="cuda") + 0 * big[0, 0] for e in elems]
+    for h, f in zip(host, fill):
+        h.copy_(f, non_blocking=True)
+    hs.run(host, 1.0, 1.0)
+    torch.cuda.synchronize()
+    for h in host:
+        assert torch.all(h == 6.0)
