@@ -542,6 +542,8 @@ def main(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="N>1: launch every step eagerly instead of as one CUDA-graph launch")
     ap.add_argument("--check", action="store_true",
                     help="after the timed region, check every segment of one more step "
                          "against the fp64 oracle (N=1)")

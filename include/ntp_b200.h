@@ -174,7 +174,10 @@ int ntp_reshard(const ntp_plan *plan, void *const *bufs, int n_bufs, void *strea
 
 /* uniform_grad_sync, tpnumerics.py:263-286, over R identically laid out local
  * replicas of n elements: sum in replica order (op SUM), true mean (MEAN) or
- * sum_r w[r]*x_r (WEIGHTED), written back to all R. */
+ * sum_r w[r]*x_r (WEIGHTED), written back to all R.  w (host memory, R
+ * doubles) is read during the call and passed to the kernel by value: no
+ * device allocation or copy per call.  128-bit vector path when every
+ * replica is 16-byte aligned. */
 int ntp_uniform_sync(void *const *reps, int R, int64_t n, int dtype, int op, const double *w,
                      void *stream);
 
@@ -337,6 +340,27 @@ int ntp_signal_post(uint64_t *const *post, int n_post, uint64_t epoch, void *str
 /* Block the stream until every word in wait[] is >= epoch (bounded spin). */
 int ntp_signal_wait(uint64_t *const *wait, int n_wait, uint64_t epoch, uint64_t spin_ns,
                     int *status, void *stream);
+
+/* Device-resident epochs: the same four calls with the epoch read on the
+ * device from *epoch_word (a u64 in device memory counting the completed
+ * steps; this launch uses *epoch_word + 1), so a step recorded once into a
+ * CUDA graph can be replayed step after step with no host involvement.  The
+ * step's final launch advances the word: ntp_grad_sync_step_dev always,
+ * ntp_signal_wait_dev when advance != 0 (the done-wait of a three-launch
+ * step); the post and signalled-sync launches only read it. */
+int ntp_grad_sync_signaled_dev(const ntp_plan *plan, void *const *bufs, int n_bufs, int op,
+                               double w_a, double w_b, uint64_t *const *wait, int n_wait,
+                               uint64_t *const *post, int n_post, uint64_t *epoch_word,
+                               uint64_t spin_ns, int *status, void *stream);
+int ntp_grad_sync_step_dev(const ntp_plan *plan, void *const *bufs, int n_bufs, int op,
+                           double w_a, double w_b, uint64_t *const *post_ready, int n_post_ready,
+                           uint64_t *const *wait_ready, int n_wait_ready,
+                           uint64_t *const *post_done, int n_post_done,
+                           uint64_t *const *wait_done, int n_wait_done, uint64_t *epoch_word,
+                           uint64_t spin_ns, int *status, void *stream);
+int ntp_signal_post_dev(uint64_t *const *post, int n_post, uint64_t *epoch_word, void *stream);
+int ntp_signal_wait_dev(uint64_t *const *wait, int n_wait, uint64_t *epoch_word, int advance,
+                        uint64_t spin_ns, int *status, void *stream);
 
 #ifdef __cplusplus
 }

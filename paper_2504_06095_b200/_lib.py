@@ -112,6 +112,19 @@ SIGNATURES = {
     "ntp_signal_post": (ctypes.c_int, [_u64pp, ctypes.c_int, ctypes.c_uint64, _vp]),
     "ntp_signal_wait": (ctypes.c_int, [_u64pp, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64,
                                        ctypes.POINTER(ctypes.c_int), _vp]),
+    "ntp_grad_sync_signaled_dev": (ctypes.c_int, [_vp, _vpp, ctypes.c_int, ctypes.c_int,
+                                                  ctypes.c_double, ctypes.c_double, _u64pp,
+                                                  ctypes.c_int, _u64pp, ctypes.c_int, _vp,
+                                                  ctypes.c_uint64, ctypes.POINTER(ctypes.c_int),
+                                                  _vp]),
+    "ntp_grad_sync_step_dev": (ctypes.c_int, [_vp, _vpp, ctypes.c_int, ctypes.c_int,
+                                              ctypes.c_double, ctypes.c_double, _u64pp,
+                                              ctypes.c_int, _u64pp, ctypes.c_int, _u64pp,
+                                              ctypes.c_int, _u64pp, ctypes.c_int, _vp,
+                                              ctypes.c_uint64, ctypes.POINTER(ctypes.c_int), _vp]),
+    "ntp_signal_post_dev": (ctypes.c_int, [_u64pp, ctypes.c_int, _vp, _vp]),
+    "ntp_signal_wait_dev": (ctypes.c_int, [_u64pp, ctypes.c_int, _vp, ctypes.c_int,
+                                           ctypes.c_uint64, ctypes.POINTER(ctypes.c_int), _vp]),
 }
 
 _lib = None

@@ -95,8 +95,7 @@ def _suite_shard_invariants(seed: int) -> dict:
 
 def _suite_tp_numerics(seed: int) -> dict:
     """cli.py:164-247: 100 nonuniform syncs (fp64, on the device) equal dense
-    sums, then 10 permuted-layout uniform syncs (attention forward is out of
-    scope: heads are sync units only)."""
+    sums, 10 permuted-layout uniform syncs, 10 head-sharded attention forwards."""
     import torch
 
     from . import tpnumerics as T
@@ -157,13 +156,109 @@ def _suite_tp_numerics(seed: int) -> dict:
             if err > 1e-12:
                 return _fail("tp-numerics", "uniform sync not invariant to shard permutation",
                              {"instance": i, "k": k, "n": n, "rel_err": err})
+    for i in range(10):  # head-sharded attention forward == dense (same rng stream)
+        heads = int(rng.integers(2, 9))
+        head_dim = int(rng.integers(2, 5))
+        hidden = int(rng.integers(3, 7))
+        n = int(rng.integers(1, heads + 1))
+        att = T.AttentionLayer.random(heads, hidden, head_dim, seed=int(rng.integers(2**31)))
+        rep = T.AttentionReplica(att, T.contiguous_assignment(heads, n), dtype=torch.float64)
+        x = rng.standard_normal((4, hidden))
+        err = _rel_err(T.attention_forward_tp(x, rep), T.attention_forward_dense(x, att))
+        worst = max(worst, err)
+        if err > 1e-12:
+            return _fail("tp-numerics", "sharded attention differs from dense",
+                         {"instance": i, "heads": heads, "n": n, "rel_err": err})
     elapsed = time.time() - start
     if elapsed > 30.0:
         return _fail("tp-numerics", f"suite exceeded 30 s budget ({elapsed:.1f} s)", {})
-    return _ok("tp-numerics", f"110 instances, worst rel err {worst:.2e}, {elapsed:.1f} s")
+    return _ok("tp-numerics", f"120 instances, worst rel err {worst:.2e}, {elapsed:.1f} s")
 
 
-SUITES = {"shard-invariants": _suite_shard_invariants, "tp-numerics": _suite_tp_numerics}
+def _central_differences(T, x, g, A, B, h: float = 1e-6):
+    """d(sum(Z * g))/dA and /dB by central differences, every entry at once:
+    the +h / -h bumps of all hidden*ffn entries of A (then of B) form one batch
+    of perturbed weight matrices evaluated by a single batched fp64 forward."""
+    import torch
+    dev = T._device()
+    X, G = T._dev64(x), T._dev64(g)
+    A, B = T._dev64(A), T._dev64(B)
+
+    def losses(As, Bs):  # As [n, h, f], Bs [n, f, h] -> [n]
+        Z = torch.matmul(T._gelu_t(torch.matmul(X, As)), Bs)
+        return (Z * G).sum(dim=(1, 2))
+    out = []
+    for W, other, first in ((A, B, True), (B, A, False)):
+        n = W.numel()
+        eye = torch.eye(n, dtype=torch.float64, device=dev).reshape(n, *W.shape) * h
+        Wp, Wm = W.unsqueeze(0) + eye, W.unsqueeze(0) - eye
+        O = other.unsqueeze(0).expand(n, *other.shape)
+        up = losses(Wp, O) if first else losses(O, Wp)
+        dn = losses(Wm, O) if first else losses(O, Wm)
+        out.append(((up - dn) / (2 * h)).reshape(W.shape).cpu().numpy())
+    return out
+
+
+def _suite_grad_finite_diff(seed: int) -> dict:
+    """cli.py:250-285: 50 random small MLPs, analytic mlp_backward (device
+    fp64) against central differences of the device forward, <= 1e-6."""
+    import torch
+
+    from . import tpnumerics as T
+    if not torch.cuda.is_available():
+        return _fail("grad-finite-diff", "needs a CUDA device (no CPU fallback)", {})
+    rng = np.random.default_rng(seed)
+    worst = 0.0
+    for i in range(50):
+        hidden = int(rng.integers(2, 6))
+        ffn = int(rng.integers(3, 11))
+        layer = T.MlpLayer.random(hidden, ffn, seed=int(rng.integers(2**31)))
+        x = rng.standard_normal((3, hidden))
+        g = rng.standard_normal((3, hidden))
+        da, db = T.mlp_backward(x, layer, g)
+        fd_a, fd_b = _central_differences(T, x, g, layer.A, layer.B)
+        err = max(_rel_err(fd_a, da), _rel_err(fd_b, db))
+        worst = max(worst, err)
+        if err > 1e-6:
+            return _fail("grad-finite-diff", "analytic gradient differs from central differences",
+                         {"instance": i, "hidden": hidden, "ffn": ffn, "rel_err": err})
+    return _ok("grad-finite-diff", f"50 instances, worst rel err {worst:.2e}")
+
+
+def _golden_fixture() -> dict:
+    """The reference's committed golden MLP fixture (configs/golden_mlp.json,
+    h=4, ffn=16, seed 0), shipped with this package."""
+    from importlib import resources
+    return json.loads(resources.files(__package__).joinpath("configs/golden_mlp.json").read_text())
+
+
+def _suite_golden(seed: int) -> dict:
+    """cli.py:288-309: the seeded layer stream reproduces the fixture's A, B;
+    the device forward and backward reproduce its Y, dA, dB within 1e-12."""
+    import torch
+
+    from . import tpnumerics as T
+    del seed  # the fixture is fixed
+    if not torch.cuda.is_available():
+        return _fail("golden", "needs a CUDA device (no CPU fallback)", {})
+    fx = _golden_fixture()
+    layer = T.MlpLayer(A=np.array(fx["A"]), B=np.array(fx["B"]))
+    regen = T.MlpLayer.random(fx["hidden"], fx["ffn"], seed=fx["seed"])
+    if not (np.array_equal(regen.A, layer.A) and np.array_equal(regen.B, layer.B)):
+        return _fail("golden", "seeded layer generation drifted from the fixture", {})
+    x, g = np.array(fx["X"]), np.array(fx["G"])
+    da, db = T.mlp_backward(x, layer, g)
+    got = {"Y": T.mlp_forward_dense(x, layer), "dA": da, "dB": db}
+    for name in ("Y", "dA", "dB"):
+        err = _rel_err(got[name], np.array(fx[name]))
+        if err > 1e-12:
+            return _fail("golden", f"recomputed {name} differs from the committed fixture",
+                         {"field": name, "rel_err": err})
+    return _ok("golden", "forward and gradients match the committed fixture")
+
+
+SUITES = {"shard-invariants": _suite_shard_invariants, "tp-numerics": _suite_tp_numerics,
+          "grad-finite-diff": _suite_grad_finite_diff, "golden": _suite_golden}
 
 
 def cmd_verify(args) -> int:

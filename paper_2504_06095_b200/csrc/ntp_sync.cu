@@ -64,6 +64,11 @@ struct SignalArgs {
   int *status;
   unsigned int *counter;  // CTA completion counter (device, zeroed)
   int wmask = 3;          // bit 0: write side A, bit 1: write side B
+  // device-resident epochs (CUDA-graph replayable steps): when set, the epoch
+  // of this launch is *epoch_word + 1 (the word counts completed steps), and
+  // the step's final kernel (advance = 1) stores that epoch back
+  uint64_t *epoch_word = nullptr;
+  int advance = 0;
 };
 
 enum { OP_COPY = 3 };
@@ -193,6 +198,16 @@ __device__ __forceinline__ uint64_t global_timer_ns() {
   return t;
 }
 
+// This launch's epoch: the host value, or (graph-replayable steps) one past
+// the device word that counts completed steps.
+__device__ __forceinline__ uint64_t sig_epoch(const SignalArgs &sig) {
+  if (!sig.epoch_word) return sig.epoch;
+  return *reinterpret_cast<volatile const uint64_t *>(sig.epoch_word) + 1;
+}
+__device__ __forceinline__ void sig_advance(const SignalArgs &sig, uint64_t e) {
+  if (sig.epoch_word && sig.advance) *reinterpret_cast<volatile uint64_t *>(sig.epoch_word) = e;
+}
+
 // Returns false on timeout (status set).
 __device__ bool wait_signals(uint64_t *const *wait, int n, uint64_t epoch, uint64_t spin_ns,
                              int *status) {
@@ -231,11 +246,14 @@ __device__ __forceinline__ unsigned int *failed_ctas(const SignalArgs &sig) { re
 // process's status reports the failure.
 __device__ __forceinline__ void last_cta_finish(const SignalArgs &sig) {
   __threadfence_system();
+  const uint64_t e = sig_epoch(sig);
   const unsigned int failed = atomicExch(failed_ctas(sig), 0u);
   *sig.counter = 0u;
-  if (failed) return;
-  for (int i = 0; i < sig.n_post; ++i) st_release_sys(sig.post[i], sig.epoch);
-  if (sig.n_fin) wait_signals(sig.fin, sig.n_fin, sig.epoch, sig.spin_ns, sig.status);
+  if (!failed) {
+    for (int i = 0; i < sig.n_post; ++i) st_release_sys(sig.post[i], e);
+    if (sig.n_fin) wait_signals(sig.fin, sig.n_fin, e, sig.spin_ns, sig.status);
+  }
+  sig_advance(sig, e);  // every CTA has read the word: it is safe to move on
 }
 
 // A CTA whose ready-wait timed out does no work but still counts itself, so
@@ -260,10 +278,11 @@ __device__ __forceinline__ bool cta_prologue(const SignalArgs &sig) {
       // the first CTA to start posts this process's ready words, so no CTA
       // waits on a post that an unscheduled CTA would make (word 1 of the
       // plan's counter block records the last epoch posted)
+      const uint64_t e = sig_epoch(sig);
       if (sig.n_pre && atomicMax(reinterpret_cast<unsigned long long *>(sig.counter) + 1,
-                                 (unsigned long long)sig.epoch) < sig.epoch)
-        post_signals(sig.pre, sig.n_pre, sig.epoch);
-      ok = wait_signals(sig.wait, sig.n_wait, sig.epoch, sig.spin_ns, sig.status) ? 1 : 0;
+                                 (unsigned long long)e) < e)
+        post_signals(sig.pre, sig.n_pre, e);
+      ok = wait_signals(sig.wait, sig.n_wait, e, sig.spin_ns, sig.status) ? 1 : 0;
     }
     __syncthreads();
     return ok != 0;
@@ -513,50 +532,99 @@ plan_kernel_scalar(const Chunk *__restrict__ chunks, int n_chunks, BufTable bufs
   cta_epilogue<kSignaled>(sig);
 }
 
-// uniform_grad_sync over R local replicas (tpnumerics.py:263-286)
+// uniform_grad_sync over R local replicas (tpnumerics.py:263-286).  Weights
+// travel by value in the launch (no device buffer, no per-call allocation).
+struct RepWeights {
+  double w[kMaxBufs];
+};
+
+template <typename T>
+__device__ __forceinline__ typename Acc<T>::type uniform_elem(const BufTable &reps, int R, int op,
+                                                              const RepWeights &w, int64_t e) {
+  using A = typename Acc<T>::type;
+  A acc;
+  if (op == NTP_OP_MEAN) {  // true mean over all replicas (tpnumerics.py:280-283)
+    acc = A(0);
+    for (int r = 0; r < R; ++r) acc = add_rn(acc, A(reinterpret_cast<const T *>(reps.p[r])[e]));
+    acc = acc / A(R);
+  } else if (op == NTP_OP_SUM) {  // replica order (tpnumerics.py:276-279)
+    acc = A(reinterpret_cast<const T *>(reps.p[0])[e]);
+    for (int r = 1; r < R; ++r) acc = add_rn(acc, A(reinterpret_cast<const T *>(reps.p[r])[e]));
+  } else {
+    acc = mul_rn(A(w.w[0]), A(reinterpret_cast<const T *>(reps.p[0])[e]));
+    for (int r = 1; r < R; ++r)
+      acc = add_rn(acc, mul_rn(A(w.w[r]), A(reinterpret_cast<const T *>(reps.p[r])[e])));
+  }
+  return acc;
+}
+
+// 16-byte vectors when every replica base is 16-byte aligned: each thread
+// reduces 16/sizeof(T) consecutive elements with 128-bit loads and stores
+// (same per-element arithmetic and order as the scalar path); the tail and
+// unaligned buffers take the scalar path.
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
-uniform_kernel(BufTable reps, int R, int64_t n, int op, BufTable wts_unused,
-               typename Acc<T>::type w0, const double *__restrict__ w) {
+uniform_kernel(BufTable reps, int R, int64_t n, int op, RepWeights w, int64_t n_vec) {
   using A = typename Acc<T>::type;
+  constexpr int kPer = 16 / sizeof(T);
   const int64_t stride = (int64_t)gridDim.x * kThreads;
-  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < n; e += stride) {
-    A acc;
-    if (op == NTP_OP_MEAN) {
-      acc = A(0);
-      for (int r = 0; r < R; ++r) acc = add_rn(acc, A(reinterpret_cast<T *>(reps.p[r])[e]));
-      acc = acc / A(R);
-    } else if (op == NTP_OP_SUM) {
-      acc = A(reinterpret_cast<T *>(reps.p[0])[e]);
-      for (int r = 1; r < R; ++r) acc = add_rn(acc, A(reinterpret_cast<T *>(reps.p[r])[e]));
-    } else {
-      acc = mul_rn(A(w[0]), A(reinterpret_cast<T *>(reps.p[0])[e]));
-      for (int r = 1; r < R; ++r)
-        acc = add_rn(acc, mul_rn(A(w[r]), A(reinterpret_cast<T *>(reps.p[r])[e])));
+  const int64_t tid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  for (int64_t v = tid; v < n_vec; v += stride) {
+    A acc[kPer];
+    {
+      const uint4 x = ld_stream(reinterpret_cast<const uint4 *>(reps.p[0]) + v);
+      const T *xe = reinterpret_cast<const T *>(&x);
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const A a = A(xe[j]);
+        acc[j] = op == NTP_OP_WEIGHTED ? mul_rn(A(w.w[0]), a)
+                 : op == NTP_OP_MEAN    ? add_rn(A(0), a)  // as the scalar path: 0 + a
+                                        : a;
+      }
     }
-    const T o = T(acc);
+    for (int r = 1; r < R; ++r) {
+      const uint4 x = ld_stream(reinterpret_cast<const uint4 *>(reps.p[r]) + v);
+      const T *xe = reinterpret_cast<const T *>(&x);
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const A a = A(xe[j]);
+        acc[j] = add_rn(acc[j], op == NTP_OP_WEIGHTED ? mul_rn(A(w.w[r]), a) : a);
+      }
+    }
+    uint4 o;
+    T *oe = reinterpret_cast<T *>(&o);
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) oe[j] = T(op == NTP_OP_MEAN ? acc[j] / A(R) : acc[j]);
+    for (int r = 0; r < R; ++r) st_stream(reinterpret_cast<uint4 *>(reps.p[r]) + v, o);
+  }
+  for (int64_t e = n_vec * kPer + tid; e < n; e += stride) {
+    const T o = T(uniform_elem<T>(reps, R, op, w, e));
     for (int r = 0; r < R; ++r) reinterpret_cast<T *>(reps.p[r])[e] = o;
   }
-  (void)wts_unused;
-  (void)w0;
 }
 
 __global__ void signal_post_kernel(SignalArgs sig) {
+  const uint64_t e = sig_epoch(sig);
   __threadfence_system();
-  for (int i = 0; i < sig.n_post; ++i) st_release_sys(sig.post[i], sig.epoch);
+  for (int i = 0; i < sig.n_post; ++i) st_release_sys(sig.post[i], e);
+  sig_advance(sig, e);
 }
 
 __global__ void signal_wait_kernel(SignalArgs sig) {
-  wait_signals(sig.wait, sig.n_wait, sig.epoch, sig.spin_ns, sig.status);
+  const uint64_t e = sig_epoch(sig);
+  wait_signals(sig.wait, sig.n_wait, e, sig.spin_ns, sig.status);
+  sig_advance(sig, e);
 }
 
 // a step with nothing to compute: post ready, wait ready, post done, wait done
 __global__ void signal_step_kernel(SignalArgs sig) {
-  post_signals(sig.pre, sig.n_pre, sig.epoch);
-  if (wait_signals(sig.wait, sig.n_wait, sig.epoch, sig.spin_ns, sig.status)) {
-    post_signals(sig.post, sig.n_post, sig.epoch);
-    wait_signals(sig.fin, sig.n_fin, sig.epoch, sig.spin_ns, sig.status);
+  const uint64_t e = sig_epoch(sig);
+  post_signals(sig.pre, sig.n_pre, e);
+  if (wait_signals(sig.wait, sig.n_wait, e, sig.spin_ns, sig.status)) {
+    post_signals(sig.post, sig.n_post, e);
+    wait_signals(sig.fin, sig.n_fin, e, sig.spin_ns, sig.status);
   }
+  sig_advance(sig, e);
 }
 
 // ---------------------------------------------------------------------------
@@ -797,24 +865,30 @@ int ntp_uniform_sync(void *const *reps, int R, int64_t n, int dtype, int op, con
   int st = set_device(attr.device);
   if (st) return st;
   BufTable bt{};
-  for (int r = 0; r < R; ++r) bt.p[r] = static_cast<char *>(reps[r]);
-  double *d_w = nullptr;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (op == NTP_OP_WEIGHTED) {
-    // weights live in a small device buffer owned by the stream's lifetime
-    NTP_CUDA(cudaMallocAsync(&d_w, sizeof(double) * R, s));
-    NTP_CUDA(cudaMemcpyAsync(d_w, w, sizeof(double) * R, cudaMemcpyHostToDevice, s));
+  bool aligned = true;
+  for (int r = 0; r < R; ++r) {
+    bt.p[r] = static_cast<char *>(reps[r]);
+    aligned &= (reinterpret_cast<uintptr_t>(reps[r]) & 15u) == 0;
   }
-  const int blocks = (int)std::min<int64_t>((n + kThreads - 1) / kThreads, sm_count(attr.device) * 8);
+  RepWeights wv{};
+  if (op == NTP_OP_WEIGHTED) {
+    if (!w) return fail(NTP_EINVAL, "weighted op needs one weight per replica");
+    for (int r = 0; r < R; ++r) wv.w[r] = w[r];
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int esize = dtype == NTP_F64 ? 8 : dtype == NTP_F32 ? 4 : 2;
+  const int64_t n_vec = aligned ? n * esize / 16 : 0;
+  const int64_t work = n_vec + (n - n_vec * 16 / esize);
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((work + kThreads - 1) / kThreads,
+                                                                 sm_count(attr.device) * 8));
   switch (dtype) {
-    case NTP_F32: uniform_kernel<float><<<blocks, kThreads, 0, s>>>(bt, R, n, op, bt, 0.f, d_w); break;
-    case NTP_BF16: uniform_kernel<__nv_bfloat16><<<blocks, kThreads, 0, s>>>(bt, R, n, op, bt, 0.f, d_w); break;
-    case NTP_F16: uniform_kernel<__half><<<blocks, kThreads, 0, s>>>(bt, R, n, op, bt, 0.f, d_w); break;
-    case NTP_F64: uniform_kernel<double><<<blocks, kThreads, 0, s>>>(bt, R, n, op, bt, 0.0, d_w); break;
+    case NTP_F32: uniform_kernel<float><<<blocks, kThreads, 0, s>>>(bt, R, n, op, wv, n_vec); break;
+    case NTP_BF16: uniform_kernel<__nv_bfloat16><<<blocks, kThreads, 0, s>>>(bt, R, n, op, wv, n_vec); break;
+    case NTP_F16: uniform_kernel<__half><<<blocks, kThreads, 0, s>>>(bt, R, n, op, wv, n_vec); break;
+    case NTP_F64: uniform_kernel<double><<<blocks, kThreads, 0, s>>>(bt, R, n, op, wv, n_vec); break;
     default: return fail(NTP_EINVAL, "unsupported dtype");
   }
   NTP_CUDA(cudaGetLastError());
-  if (d_w) NTP_CUDA(cudaFreeAsync(d_w, s));
   return NTP_OK;
 }
 
@@ -881,10 +955,10 @@ static int fill_signals(SignalArgs &sig, uint64_t *const *wait, int n_wait, uint
   return NTP_OK;
 }
 
-int ntp_grad_sync_signaled(const ntp_plan *p, void *const *bufs, int n_bufs, int op, double w_a,
-                           double w_b, uint64_t *const *wait, int n_wait, uint64_t *const *post,
-                           int n_post, uint64_t epoch, uint64_t spin_ns, int *status,
-                           void *stream) {
+static int grad_sync_signaled(const ntp_plan *p, void *const *bufs, int n_bufs, int op,
+                              double w_a, double w_b, uint64_t *const *wait, int n_wait,
+                              uint64_t *const *post, int n_post, uint64_t epoch,
+                              uint64_t *epoch_word, uint64_t spin_ns, int *status, void *stream) {
   BufTable bt;
   int st = check_exec(p, bufs, n_bufs, bt);
   if (st) return st;
@@ -893,6 +967,7 @@ int ntp_grad_sync_signaled(const ntp_plan *p, void *const *bufs, int n_bufs, int
   SignalArgs sig;
   if ((st = fill_signals(sig, wait, n_wait, post, n_post, epoch, spin_ns, status))) return st;
   sig.counter = p->d_counter;
+  sig.epoch_word = epoch_word;  // never advanced here: the step's done-wait advances
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (p->chunks.empty()) {
     signal_wait_kernel<<<1, 1, 0, s>>>(sig);
@@ -905,11 +980,29 @@ int ntp_grad_sync_signaled(const ntp_plan *p, void *const *bufs, int n_bufs, int
   return NTP_OK;
 }
 
-int ntp_grad_sync_step(const ntp_plan *p, void *const *bufs, int n_bufs, int op, double w_a,
-                       double w_b, uint64_t *const *post_ready, int n_post_ready,
-                       uint64_t *const *wait_ready, int n_wait_ready, uint64_t *const *post_done,
-                       int n_post_done, uint64_t *const *wait_done, int n_wait_done,
-                       uint64_t epoch, uint64_t spin_ns, int *status, void *stream) {
+int ntp_grad_sync_signaled(const ntp_plan *p, void *const *bufs, int n_bufs, int op, double w_a,
+                           double w_b, uint64_t *const *wait, int n_wait, uint64_t *const *post,
+                           int n_post, uint64_t epoch, uint64_t spin_ns, int *status,
+                           void *stream) {
+  return grad_sync_signaled(p, bufs, n_bufs, op, w_a, w_b, wait, n_wait, post, n_post, epoch,
+                            nullptr, spin_ns, status, stream);
+}
+
+int ntp_grad_sync_signaled_dev(const ntp_plan *p, void *const *bufs, int n_bufs, int op,
+                               double w_a, double w_b, uint64_t *const *wait, int n_wait,
+                               uint64_t *const *post, int n_post, uint64_t *epoch_word,
+                               uint64_t spin_ns, int *status, void *stream) {
+  if (!epoch_word) return fail(NTP_EINVAL, "epoch_word is required");
+  return grad_sync_signaled(p, bufs, n_bufs, op, w_a, w_b, wait, n_wait, post, n_post, 0,
+                            epoch_word, spin_ns, status, stream);
+}
+
+static int grad_sync_step(const ntp_plan *p, void *const *bufs, int n_bufs, int op, double w_a,
+                          double w_b, uint64_t *const *post_ready, int n_post_ready,
+                          uint64_t *const *wait_ready, int n_wait_ready,
+                          uint64_t *const *post_done, int n_post_done,
+                          uint64_t *const *wait_done, int n_wait_done, uint64_t epoch,
+                          uint64_t *epoch_word, uint64_t spin_ns, int *status, void *stream) {
   if (n_post_ready < 0 || n_post_ready > 16 || n_wait_done < 0 || n_wait_done > 16)
     return fail(NTP_EINVAL, "at most 16 wait and 16 post signals");
   SignalArgs sig;
@@ -920,6 +1013,8 @@ int ntp_grad_sync_step(const ntp_plan *p, void *const *bufs, int n_bufs, int op,
   for (int i = 0; i < n_wait_done; ++i) sig.fin[i] = wait_done[i];
   sig.n_pre = n_post_ready;
   sig.n_fin = n_wait_done;
+  sig.epoch_word = epoch_word;
+  sig.advance = 1;  // one launch is the whole step
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (!p || p->chunks.empty()) {
     if ((st = p ? set_device(p->device) : set_device_of(s))) return st;
@@ -937,25 +1032,71 @@ int ntp_grad_sync_step(const ntp_plan *p, void *const *bufs, int n_bufs, int op,
   return NTP_OK;
 }
 
-int ntp_signal_post(uint64_t *const *post, int n_post, uint64_t epoch, void *stream) {
+int ntp_grad_sync_step(const ntp_plan *p, void *const *bufs, int n_bufs, int op, double w_a,
+                       double w_b, uint64_t *const *post_ready, int n_post_ready,
+                       uint64_t *const *wait_ready, int n_wait_ready, uint64_t *const *post_done,
+                       int n_post_done, uint64_t *const *wait_done, int n_wait_done,
+                       uint64_t epoch, uint64_t spin_ns, int *status, void *stream) {
+  return grad_sync_step(p, bufs, n_bufs, op, w_a, w_b, post_ready, n_post_ready, wait_ready,
+                        n_wait_ready, post_done, n_post_done, wait_done, n_wait_done, epoch,
+                        nullptr, spin_ns, status, stream);
+}
+
+int ntp_grad_sync_step_dev(const ntp_plan *p, void *const *bufs, int n_bufs, int op, double w_a,
+                           double w_b, uint64_t *const *post_ready, int n_post_ready,
+                           uint64_t *const *wait_ready, int n_wait_ready,
+                           uint64_t *const *post_done, int n_post_done,
+                           uint64_t *const *wait_done, int n_wait_done, uint64_t *epoch_word,
+                           uint64_t spin_ns, int *status, void *stream) {
+  if (!epoch_word) return fail(NTP_EINVAL, "epoch_word is required");
+  return grad_sync_step(p, bufs, n_bufs, op, w_a, w_b, post_ready, n_post_ready, wait_ready,
+                        n_wait_ready, post_done, n_post_done, wait_done, n_wait_done, 0,
+                        epoch_word, spin_ns, status, stream);
+}
+
+static int signal_post(uint64_t *const *post, int n_post, uint64_t epoch, uint64_t *epoch_word,
+                       void *stream) {
   SignalArgs sig;
   int st = fill_signals(sig, nullptr, 0, post, n_post, epoch, 0, nullptr);
   if (st) return st;
+  sig.epoch_word = epoch_word;
   if ((st = set_device_of(static_cast<cudaStream_t>(stream)))) return st;
   signal_post_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(sig);
   NTP_CUDA(cudaGetLastError());
   return NTP_OK;
 }
 
-int ntp_signal_wait(uint64_t *const *wait, int n_wait, uint64_t epoch, uint64_t spin_ns,
-                    int *status, void *stream) {
+static int signal_wait(uint64_t *const *wait, int n_wait, uint64_t epoch, uint64_t *epoch_word,
+                       int advance, uint64_t spin_ns, int *status, void *stream) {
   SignalArgs sig;
   int st = fill_signals(sig, wait, n_wait, nullptr, 0, epoch, spin_ns, status);
   if (st) return st;
+  sig.epoch_word = epoch_word;
+  sig.advance = advance ? 1 : 0;
   if ((st = set_device_of(static_cast<cudaStream_t>(stream)))) return st;
   signal_wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(sig);
   NTP_CUDA(cudaGetLastError());
   return NTP_OK;
+}
+
+int ntp_signal_post(uint64_t *const *post, int n_post, uint64_t epoch, void *stream) {
+  return signal_post(post, n_post, epoch, nullptr, stream);
+}
+
+int ntp_signal_wait(uint64_t *const *wait, int n_wait, uint64_t epoch, uint64_t spin_ns,
+                    int *status, void *stream) {
+  return signal_wait(wait, n_wait, epoch, nullptr, 0, spin_ns, status, stream);
+}
+
+int ntp_signal_post_dev(uint64_t *const *post, int n_post, uint64_t *epoch_word, void *stream) {
+  if (!epoch_word) return fail(NTP_EINVAL, "epoch_word is required");
+  return signal_post(post, n_post, 0, epoch_word, stream);
+}
+
+int ntp_signal_wait_dev(uint64_t *const *wait, int n_wait, uint64_t *epoch_word, int advance,
+                        uint64_t spin_ns, int *status, void *stream) {
+  if (!epoch_word) return fail(NTP_EINVAL, "epoch_word is required");
+  return signal_wait(wait, n_wait, 0, epoch_word, advance, spin_ns, status, stream);
 }
 
 }  // extern "C"

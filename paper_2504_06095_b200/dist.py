@@ -235,11 +235,20 @@ class NtpSyncGroup:
 
     def __init__(self, lay: PairLayout, placement: Placement, dtype: torch.dtype, device: int,
                  ops: DeviceOps | None = None, group=None, policy: str = "split",
-                 pieces=None):
+                 pieces=None, aligned: str = "peer"):
         """pieces: optional list of segment-index lists.  Each piece gets its
         own plan, so a caller can sync piece i as soon as its gradients (or its
         host-to-device copies) are in place: ``step(..., piece=i)``.  Every
-        process must step the pieces in the same order (epochs pair up)."""
+        process must step the pieces in the same order (epochs pair up).
+
+        aligned: with n1 == n2 the two replicas' shards line up (comp layout ==
+        sync layout, identical arenas per rank pair); "nccl" then syncs each
+        healthy/reduced arena pair with an NCCL all-reduce (aligned_all_reduce,
+        the fall-through of uniform_grad_sync, tpnumerics.py:263-286) instead
+        of the peer-memory kernel; "peer" (default, measured faster on B200:
+        DESIGN.md 5) keeps the kernel.  Ignored when n1 != n2."""
+        if aligned not in ("peer", "nccl"):
+            raise ValueError(f"aligned must be 'peer' or 'nccl', got {aligned!r}")
         self.pieces = [sorted(int(i) for i in p) for p in pieces] if pieces else []
         for p in self.pieces:
             if not p or p != list(range(p[0], p[-1] + 1)):
@@ -288,6 +297,8 @@ class NtpSyncGroup:
         self.fused_step = False
         self._sig_arrays = None
         self._bufs_array = None
+        self.aligned = aligned if lay.n1 == lay.n2 else "peer"
+        self._aligned_pairs = self._aligned_groups(group) if self.aligned == "nccl" else None
 
     def _build_plans(self, policy) -> None:
         """What this process computes under an executor policy, which peer
@@ -329,6 +340,50 @@ class NtpSyncGroup:
             self.piece_plans.append(pp.finalize())
         self.policy = policy
 
+    def _aligned_groups(self, group):
+        """(healthy slot, reduced slot, 2-process NCCL group or None when both
+        slots live in this process) for every aligned pair this process hosts.
+        new_group is collective: every process creates every pair's group, in
+        ascending pair order."""
+        n1, plc = self.lay.n1, self.plc
+        ranks = dist.get_process_group_ranks(group) if group is not None else list(range(self.world))
+        groups = {}
+        for i in range(n1):
+            p, q = plc.proc_of_slot(i), plc.proc_of_slot(i + n1)
+            key = (min(p, q), max(p, q))
+            if p != q and key not in groups:
+                groups[key] = dist.new_group([ranks[key[0]], ranks[key[1]]])
+        pairs = []
+        for i in range(n1):
+            p, q = plc.proc_of_slot(i), plc.proc_of_slot(i + n1)
+            if self.rank in (p, q):
+                pairs.append((i, i + n1, None if p == q else groups[(min(p, q), max(p, q))]))
+        return pairs
+
+    def _step_aligned(self, w_h: float, w_r: float, stream, piece) -> None:
+        """n1 == n2 with aligned="nccl": per rank pair, one NCCL all-reduce of the
+        (piece's range of the) two identical arenas, each side pre-weighted."""
+        n1 = self.lay.n1
+        with torch.cuda.stream(stream):
+            for hs, rs, grp in self._aligned_pairs:
+                rng = self.piece_ranges(piece) if piece is not None else None
+                if grp is None:  # both copies in this process: one local 2-way kernel
+                    a, b = self.arena(hs), self.arena(rs)
+                    if rng is not None:
+                        a, b = a[slice(*rng[hs])], b[slice(*rng[rs])]
+                    L = _lib.load()
+                    w = (ctypes.c_double * 2)(float(w_h), float(w_r))
+                    _lib.check(L.ntp_uniform_sync(_lib.ptr_array([a.data_ptr(), b.data_ptr()]), 2,
+                                                  a.numel(), dtype_code(a.dtype), OPS["weighted"],
+                                                  w, ctypes.c_void_p(stream.cuda_stream)),
+                               "ntp_uniform_sync")
+                    continue
+                slot = hs if hs in self.local else rs
+                t = self.arena(slot)
+                if rng is not None:
+                    t = t[slice(*rng[slot])]
+                aligned_all_reduce(t, w_h if slot < n1 else w_r, group=grp)
+
     def set_policy(self, policy) -> "NtpSyncGroup":
         """Rebuild the plans for another executor policy (same arenas, same
         partners and signals); uploads them if the group was uploaded."""
@@ -347,6 +402,10 @@ class NtpSyncGroup:
             if pp is not None:
                 pp.upload(self.device)
         self._status = torch.zeros(1, dtype=torch.int32, device=f"cuda:{self.device}")
+        # device-resident epoch word (completed steps) for graph-replayed steps
+        self._epoch_word = torch.zeros(1, dtype=torch.int64, device=f"cuda:{self.device}")
+        self._word_epoch = 0   # the value the word holds once queued work has run
+        self._graphs = {}
         return self
 
     def arena(self, slot: int) -> torch.Tensor:
@@ -375,6 +434,9 @@ class NtpSyncGroup:
         self.epoch += 1
         e = self.epoch
         s = torch.cuda.current_stream(self.device) if stream is None else stream
+        if self.aligned == "nccl":
+            self._step_aligned(w_h, w_r, s, piece)
+            return
         sp = ctypes.c_void_p(s.cuda_stream)
         st = ctypes.cast(self._status.data_ptr(), ctypes.POINTER(ctypes.c_int))
         if self._sig_arrays is None:  # ctypes arrays built once (host cost per step)
@@ -411,6 +473,88 @@ class NtpSyncGroup:
         if self.wait_done:
             _lib.check(L.ntp_signal_wait(wd, len(self.wait_done), e, spin_ns, st, sp),
                        "ntp_signal_wait")
+
+    # -- CUDA-graph steps ------------------------------------------------------
+
+    def _launch_dev(self, w_h: float, w_r: float, s, piece) -> None:
+        """The step's launches with device-resident epochs (what step_graph
+        records): the same kernels and handshakes as step(), each reading its
+        epoch from the group's epoch word; the step's last launch advances it."""
+        L = _lib.load()
+        plan = self.plan if piece is None else self.piece_plans[piece]
+        sp = ctypes.c_void_p(s.cuda_stream)
+        st = ctypes.cast(self._status.data_ptr(), ctypes.POINTER(ctypes.c_int))
+        ew = ctypes.c_void_p(self._epoch_word.data_ptr())
+        if self._sig_arrays is None:
+            self._sig_arrays = tuple(_lib.u64_ptr_array(w) for w in
+                                     (self.post_ready, self.wait_ready, self.post_done,
+                                      self.wait_done))
+        pr, wr, pd, wd = self._sig_arrays
+        if self._bufs_array is None:
+            self._bufs_array = _lib.ptr_array(self.bufs)
+        bufs, spin = self._bufs_array, int(self._spin_ns)
+        if not self.partners:
+            if plan is not None:
+                plan.grad_sync(self.bufs, OPS["weighted"], w_h, w_r, s)
+            return
+        if self.fused_step:
+            _lib.check(L.ntp_grad_sync_step_dev(
+                plan._h if plan is not None else None, bufs, len(self.bufs), OPS["weighted"],
+                float(w_h), float(w_r), pr, len(self.post_ready), wr, len(self.wait_ready),
+                pd, len(self.post_done), wd, len(self.wait_done), ew, spin, st, sp),
+                "ntp_grad_sync_step_dev")
+            return
+        if self.post_ready:
+            _lib.check(L.ntp_signal_post_dev(pr, len(self.post_ready), ew, sp), "ntp_signal_post_dev")
+        if plan is not None:
+            _lib.check(L.ntp_grad_sync_signaled_dev(
+                plan._h, bufs, len(self.bufs), OPS["weighted"], float(w_h), float(w_r),
+                wr, len(self.wait_ready), pd, len(self.post_done), ew, spin, st, sp),
+                "ntp_grad_sync_signaled_dev")
+        else:
+            _lib.check(L.ntp_signal_wait_dev(wr, len(self.wait_ready), ew, 0, spin, st, sp),
+                       "ntp_signal_wait_dev")
+            _lib.check(L.ntp_signal_post_dev(pd, len(self.post_done), ew, sp), "ntp_signal_post_dev")
+        _lib.check(L.ntp_signal_wait_dev(wd, len(self.wait_done), ew, 1, spin, st, sp),
+                   "ntp_signal_wait_dev")
+
+    _spin_ns = 20_000_000_000
+
+    def step_graph(self, w_h: float, w_r: float, stream=None, piece: int | None = None,
+                   steps: int = 1, prologue=None) -> None:
+        """`steps` synchronisations as ONE CUDA-graph launch (recorded on first
+        use for this (piece, weights, steps, launch variant), replayed after):
+        the host cost of a step drops to one graph launch, and on the device
+        the step's kernels run back to back.  Same kernels, signals and
+        results as step(); each process must issue the same sequence of steps
+        (graph or not) so that epochs pair up.  prologue: optional callable
+        recorded before each step (e.g. a benchmark's L2 flush)."""
+        if self.aligned == "nccl":
+            for _ in range(steps):
+                self.step(w_h, w_r, stream, piece=piece)
+            return
+        s = torch.cuda.current_stream(self.device) if stream is None else stream
+        key = (piece, float(w_h), float(w_r), int(steps), bool(self.fused_step), prologue)
+        g = self._graphs.get(key)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream(self.device)
+            cap.wait_stream(s)
+            with torch.cuda.graph(g, stream=cap, capture_error_mode="thread_local"):
+                for _ in range(steps):
+                    if prologue is not None:
+                        prologue()
+                    self._launch_dev(w_h, w_r, cap, piece)
+            s.wait_stream(cap)
+            self._graphs[key] = g
+        if self._word_epoch != self.epoch:  # eager steps ran since: re-base the word
+            with torch.cuda.stream(s):
+                self._epoch_word.fill_(self.epoch)
+            self._word_epoch = self.epoch
+        with torch.cuda.stream(s):
+            g.replay()
+        self.epoch += steps
+        self._word_epoch = self.epoch
 
     def open_slots(self, slots) -> list:
         """Device pointers of the given logical slots (IPC-mapping peers' arenas

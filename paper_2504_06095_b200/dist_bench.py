@@ -58,43 +58,60 @@ def run(args):
     stream = torch.cuda.current_stream()
     torch.cuda.synchronize()
     dist.barrier()
+    # small workloads would stay L2-resident between steps: flush (256 MB
+    # write) before every timed step; the flushes are timed alone afterwards
+    # and subtracted
+    hosted_bytes = sum(grp.slot_elems[s] for s in grp.hosted) * eb
+    flush = (torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+             if 2 * lay.elems * eb <= 2 * L2_BYTES else None)
+    flush_fn = (lambda: flush.fill_(1)) if flush is not None else None  # noqa: E731
+    use_graph = not getattr(args, "no_graph", False)
+
+    def one():
+        # one step as one CUDA-graph launch (recorded during warm-up): the
+        # host's launch rate never paces the device (it would at small sizes)
+        if use_graph:
+            grp.step_graph(W_H, W_R, stream, prologue=flush_fn)
+        else:
+            if flush_fn is not None:
+                flush_fn()
+            grp.step(W_H, W_R, stream)
+
     for _ in range(max(args.warmup, 3)):
-        grp.step(W_H, W_R, stream)
+        one()
     torch.cuda.synchronize()
     dist.barrier()
     if grp.status() != 0:
         raise RuntimeError(f"rank {rank}: signal timeout during warm-up")
-    # small workloads would stay L2-resident between steps: flush (256 MB
-    # write) before every timed step, and time the steps alone
-    hosted_bytes = sum(grp.slot_elems[s] for s in grp.hosted) * eb
-    flush = (torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-             if 2 * lay.elems * eb <= 2 * L2_BYTES else None)
     clocks = ClockSampler(local)
     clocks.start()
     nv = NvlinkCounters(local)
-    nev = 2 * (args.steps if flush is not None else 1)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(nev)]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     dist.barrier()
     clocks.mark("t0")
     nv.start()
-    if flush is None:
-        ev[0].record(stream)
-        for _ in range(args.steps):
-            grp.step(W_H, W_R, stream)
-        ev[1].record(stream)
-    else:
-        for i in range(args.steps):
-            flush.fill_(i & 0xFF)
-            ev[2 * i].record(stream)
-            grp.step(W_H, W_R, stream)
-            ev[2 * i + 1].record(stream)
+    e0.record(stream)
+    for _ in range(args.steps):
+        one()
+    e1.record(stream)
     torch.cuda.synchronize()
     nvl = nv.stop()
     clocks.mark("t1")
     dist.barrier()
     clk = clocks.stop()
-    ms = _max(sum(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(nev // 2)) / args.steps)
+    total_ms = e0.elapsed_time(e1)
+    flush_ms = 0.0
+    if flush is not None:
+        for _ in range(3):
+            flush_fn()
+        e0.record(stream)
+        for _ in range(args.steps):
+            flush_fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        flush_ms = e0.elapsed_time(e1)
+    ms = _max((total_ms - flush_ms) / args.steps)
     # NVLink bytes per step, per direction, busiest rank (NVML counters read
     # around the timed region)
     tx = _max(float(nvl["tx_bytes"]) / args.steps if nvl["tx_bytes"] is not None else -1.0)
@@ -131,6 +148,9 @@ def run(args):
                             "traffic_over_algorithmic": (round(traffic / B, 3) if traffic and B
                                                          else None),
                             "kernel_ms": round(kernel_ms, 4)},
+               "timing": ("K steps, each one CUDA-graph launch" if use_graph else "K eager steps")
+                         + (" after a 256 MB L2 flush; K flushes timed alone and subtracted"
+                            if flush is not None else ""),
                "gpu_launches": args.steps * _launches_per_step(grp),
                "clocks": clk, "e2e": e2e}
     dist.barrier()

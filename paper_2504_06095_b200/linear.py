@@ -152,15 +152,21 @@ class MlpShard:
         self.W = torch.from_numpy(w).to(device=device, dtype=torch.bfloat16)
         self.H = self.Y = None
 
-    def forward(self, X: torch.Tensor, Z: torch.Tensor, accumulate: bool = False) -> None:
-        """H = X A_i, Y = GeLU(H) (fused epilogue), Z (+)= Y B_i (fp32 partial)."""
+    def activations(self, X: torch.Tensor) -> None:
+        """H = X A_i and Y = GeLU(H) (one GEMM, fused GeLU epilogue) -- what
+        backward() needs from the forward pass."""
         T = X.shape[0]
         npad = _pad8(self.n)
         if self.H is None or self.H.shape[0] != T:
             self.H = torch.empty((T, npad), dtype=torch.bfloat16, device=X.device)
             self.Y = torch.empty((T, npad), dtype=torch.bfloat16, device=X.device)
-        H, Y = self.H[:, :self.n], self.Y[:, :self.n]
-        mm(X, self.W[:, 0, :], Y, epilogue="gelu", aux=H)
+        mm(X, self.W[:, 0, :], self.Y[:, :self.n], epilogue="gelu", aux=self.H[:, :self.n])
+
+    def forward(self, X: torch.Tensor, Z: torch.Tensor, accumulate: bool = False) -> None:
+        """H = X A_i, Y = GeLU(H) (fused epilogue), Z (+)= Y B_i (fp32 partial)."""
+        T = X.shape[0]
+        self.activations(X)
+        Y = self.Y[:, :self.n]
         if accumulate:
             part = torch.empty((T, self.h), dtype=torch.float32, device=X.device)
             mm(Y, self.W[:, 1, :].T, part)

@@ -36,7 +36,7 @@ SQRT_2_OVER_PI = float(np.sqrt(2.0 / np.pi))   # tpnumerics.py:22
 
 @dataclass(frozen=True)
 class MlpLayer:
-    """One MLP block, A [hidden x ffn], B [ffn x hidden] (tpnumerics.py:39-67)."""
+    """One MLP block, A [hidden x ffn], B [ffn x hidden] (tpnumerics.py:40-67)."""
 
     A: np.ndarray
     B: np.ndarray
@@ -85,10 +85,13 @@ class MlpReplica:
 
     Mirrors tpnumerics.py:131-155.  ``grads[r]`` is the [n_r, 2, hidden]
     device tensor; ``grad_a``/``grad_b`` are None until gradients are set
-    (``set_grads`` or ``mlp_backward_tp``), as in the reference.
+    (``set_grads`` or ``mlp_backward_tp``), as in the reference.  The default
+    gradient dtype is float64, the reference's (its inputs are cast up,
+    tpnumerics.py:47-48), so the reference's own call sites keep their 1e-12
+    tolerances; bf16 / fp32 replicas are the training-time layouts.
     """
 
-    def __init__(self, layer: MlpLayer, assignment, *, dtype: torch.dtype = torch.float32,
+    def __init__(self, layer: MlpLayer, assignment, *, dtype: torch.dtype = torch.float64,
                  device: int | str | torch.device | None = None):
         cols = np.concatenate([np.asarray(a, dtype=np.int64) for a in assignment])
         if len(cols) != layer.ffn or len(np.unique(cols)) != layer.ffn:
@@ -109,6 +112,16 @@ class MlpReplica:
     @property
     def hidden(self) -> int:
         return self.layer.hidden
+
+    @property
+    def a_frags(self) -> list[np.ndarray]:
+        """Per-rank weight fragments A[:, cols_r] [hidden, n_r] (tpnumerics.py:141)."""
+        return [self.layer.A[:, c] for c in self.cols]
+
+    @property
+    def b_frags(self) -> list[np.ndarray]:
+        """Per-rank weight fragments B[cols_r, :] [n_r, hidden] (tpnumerics.py:142)."""
+        return [self.layer.B[c, :] for c in self.cols]
 
     @property
     def grad_a(self):
@@ -160,11 +173,34 @@ class MlpReplica:
 
 
 # ---------------------------------------------------------------------------
-# gradient producer (device).  The weight-gradient GEMMs of tpnumerics.py:238-252
-# written straight into the unit-major layout the sync consumes.
+# dense / TP forward and backward (tpnumerics.py:25-36, 168-252), on the device.
+# Inputs may be numpy arrays (the reference's callers) or tensors; numpy in,
+# numpy out.  float64 work runs as fp64 device math (bit-for-bit the same
+# formulas, BLAS-order differences only, <= 1e-12 like the reference's own
+# tolerances); bf16 replicas run the tcgen05 GEMMs of linear.py.
+
+
+def _device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2504_06095_b200 computes on a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _dev64(x, device=None) -> torch.Tensor:
+    dev = _device() if device is None else device
+    if torch.is_tensor(x):
+        return x.to(device=dev, dtype=torch.float64)
+    return torch.as_tensor(np.asarray(x, dtype=np.float64), device=dev)
+
+
+def _out(t: torch.Tensor, like):
+    return t if torch.is_tensor(like) else t.cpu().numpy()
 
 
 def _gelu_t(x):
+    # GELU_C read at call time: a caller that patches the module constant (the
+    # reference's drift test, test_tpnumerics.py / cli verify --suite golden)
+    # sees the change, as with the reference's gelu
     return 0.5 * x * (1.0 + torch.tanh(SQRT_2_OVER_PI * (x + GELU_C * x**3)))
 
 
@@ -175,21 +211,94 @@ def _gelu_grad_t(x):
     return 0.5 * (1.0 + t) + 0.5 * x * (1.0 - t**2) * du
 
 
+def gelu(x):
+    """tanh-approximation GeLU (tpnumerics.py:25-28), float64."""
+    return _out(_gelu_t(_dev64(x)), x)
+
+
+def gelu_grad(x):
+    """d GeLU / dx (tpnumerics.py:31-36), float64."""
+    return _out(_gelu_grad_t(_dev64(x)), x)
+
+
+def _check_features(X, hidden: int) -> None:
+    if X.shape[1] != hidden:
+        raise ValueError(f"X has {X.shape[1]} features, layer expects {hidden}")
+
+
+def mlp_forward_dense(X, layer: MlpLayer):
+    """Z = GeLU(X A) B (tpnumerics.py:170-174)."""
+    Xd = _dev64(X)
+    _check_features(Xd, layer.hidden)
+    return _out(_gelu_t(Xd @ _dev64(layer.A)) @ _dev64(layer.B), X)
+
+
+def _shards(replica: MlpReplica):
+    """tcgen05 weight shards (unit-major bf16) of a replica, built once."""
+    from .linear import MlpShard
+    sh = getattr(replica, "_shards", None)
+    if sh is None:
+        sh = [MlpShard(replica.layer.A, replica.layer.B, c, device=replica.device)
+              for c in replica.cols]
+        replica._shards = sh
+    return sh
+
+
+def mlp_forward_tp(X, replica: MlpReplica):
+    """Sum of the per-rank partial outputs GeLU(X A_r) B_r in ascending rank
+    order (tpnumerics.py:177-185).  bf16 replicas: the tcgen05 column- then
+    row-parallel GEMMs (bf16 operands, fp32 partial sums; linear.py);
+    otherwise float64."""
+    Xd = _dev64(X, replica.device)
+    _check_features(Xd, replica.hidden)
+    if replica.dtype == torch.bfloat16:
+        from .linear import mlp_forward_tp as fwd
+        return _out(fwd(Xd.to(torch.bfloat16), _shards(replica)).double(), X)
+    A, B = _dev64(replica.layer.A, replica.device), _dev64(replica.layer.B, replica.device)
+    Z = torch.zeros((Xd.shape[0], replica.hidden), dtype=torch.float64, device=replica.device)
+    for cols in replica.cols:
+        idx = torch.as_tensor(cols, device=replica.device)
+        Z += _gelu_t(Xd @ A[:, idx]) @ B[idx, :]
+    return _out(Z, X)
+
+
+def mlp_backward(X, layer: MlpLayer, upstream_grad):
+    """Dense parameter gradients (dA [h, ffn], dB [ffn, h]) of Z = GeLU(X A) B
+    (tpnumerics.py:220-235): dB = GeLU(XA)^T G, dA = X^T((G B^T) * GeLU'(XA))."""
+    Xd, G = _dev64(X), _dev64(upstream_grad)
+    if tuple(G.shape) != (Xd.shape[0], layer.hidden):
+        raise ValueError(f"upstream grad shape {tuple(G.shape)} != {(Xd.shape[0], layer.hidden)}")
+    A, B = _dev64(layer.A), _dev64(layer.B)
+    H = Xd @ A
+    dB = _gelu_t(H).T @ G
+    dA = Xd.T @ ((G @ B.T) * _gelu_grad_t(H))
+    return _out(dA, X), _out(dB, X)
+
+
 def mlp_backward_tp(X, replica: MlpReplica, upstream_grad) -> None:
     """Per-rank dB_r = GeLU(X A_r)^T G, dA_r = X^T((G B_r^T) * GeLU'(X A_r))
-    (tpnumerics.py:238-252), computed on the replica's device in fp64 and
-    stored unit-major in the replica's gradient dtype."""
+    (tpnumerics.py:238-252), stored unit-major in the replica's arenas.
+
+    bf16 replicas run the tcgen05 GEMMs (linear.MlpShard: forward for H/Y, then
+    the dGeLU and the two weight-gradient GEMMs writing the arena in place);
+    fp32 / fp64 replicas are computed in float64 and stored in their dtype."""
     dev = replica.device
-    X = torch.as_tensor(np.asarray(X, dtype=np.float64), device=dev)
-    G = torch.as_tensor(np.asarray(upstream_grad, dtype=np.float64), device=dev)
-    A = torch.as_tensor(replica.layer.A, device=dev)
-    B = torch.as_tensor(replica.layer.B, device=dev)
+    if replica.dtype == torch.bfloat16:
+        Xb = _dev64(X, dev).to(torch.bfloat16)
+        Gb = _dev64(upstream_grad, dev).to(torch.bfloat16)
+        for sh, g in zip(_shards(replica), replica.grads):
+            sh.activations(Xb)
+            sh.backward(Xb, Gb, g)
+        replica._has_grads = True
+        return
+    Xd, G = _dev64(X, dev), _dev64(upstream_grad, dev)
+    A, B = _dev64(replica.layer.A, dev), _dev64(replica.layer.B, dev)
     for g, cols in zip(replica.grads, replica.cols):
         idx = torch.as_tensor(cols, device=dev)
         A_i, B_i = A[:, idx], B[idx, :]
-        H_i = X @ A_i
+        H_i = Xd @ A_i
         g[:, 1, :].copy_((_gelu_t(H_i).T @ G).to(replica.dtype))
-        g[:, 0, :].copy_((X.T @ ((G @ B_i.T) * _gelu_grad_t(H_i))).T.to(replica.dtype))
+        g[:, 0, :].copy_((Xd.T @ ((G @ B_i.T) * _gelu_grad_t(H_i))).T.to(replica.dtype))
     replica._has_grads = True
 
 
@@ -273,28 +382,64 @@ def nonuniform_grad_sync(healthy, reduced, smap: ShardMap, op: str = "sum",
     plan.grad_sync(tensor_ptrs(healthy.grads + reduced.grads), code, w_h, w_r)
 
 
+class _HostPath:
+    """Device resources of the reference-object path for one (layout, hidden):
+    the fp64 plan (built and uploaded once), pinned unit-major staging buffers
+    and device arenas, all reused call after call."""
+
+    def __init__(self, healthy, reduced, k: int, device: torch.device):
+        h = healthy.layer.hidden
+        self.h = h
+        self.device = device
+        plan = build_pair_plan(healthy.cols, reduced.cols, k, 2 * h, _lib.NTP_F64)
+        self.plan = plan.finalize().upload(device.index)
+        sizes = [len(c) for c in list(healthy.cols) + list(reduced.cols)]
+        self.host = [torch.empty((n, 2 * h), dtype=torch.float64).pin_memory() for n in sizes]
+        self.dev = [torch.empty((n, 2 * h), dtype=torch.float64, device=device) for n in sizes]
+        self.ptrs = tensor_ptrs(self.dev)
+        self.stream = torch.cuda.Stream(device)
+        self.bytes = sum(n * 2 * h * 8 for n in sizes)
+
+    def run(self, healthy, reduced, code, w_h, w_r) -> None:
+        h = self.h
+        frags = [(ga, gb) for rep in (healthy, reduced) for ga, gb in zip(rep.grad_a, rep.grad_b)]
+        stage = [t.numpy() for t in self.host]
+        for st, (ga, gb) in zip(stage, frags):   # reference layout -> unit-major (host)
+            st[:, :h] = np.asarray(ga).T
+            st[:, h:] = gb
+        s = self.stream
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            for d, t in zip(self.dev, self.host):
+                d.copy_(t, non_blocking=True)
+            self.plan.grad_sync(self.ptrs, code, w_h, w_r, s)
+            for d, t in zip(self.dev, self.host):
+                t.copy_(d, non_blocking=True)
+        s.synchronize()
+        for st, (ga, gb) in zip(stage, frags):   # back into the caller's arrays, in place
+            ga[...] = st[:, :h].T
+            gb[...] = st[:, h:]
+
+
+_HOST_PATHS: dict = {}
+
+
 def _nonuniform_host(healthy, reduced, smap, code, w_h, w_r) -> None:
-    """Reference-object path: numpy fp64 fragments in, numpy fragments out (in
-    place), H2D + kernel + D2H.  fp64 keeps parity with the reference bit-exact
-    for op sum/mean."""
-    h = healthy.layer.hidden
+    """Reference-object path (numpy fp64 fragments in the reference's shapes,
+    mutated in place like tpnumerics.py:346-356): pinned staging -> one H2D per
+    rank -> the fp64 sync kernel -> D2H -> the caller's arrays.  The plan, the
+    pinned staging and the device arenas are cached per layout, so repeated
+    calls (a training loop) allocate nothing.  fp64 keeps the result bit-exact
+    with the reference for op sum/mean."""
     dev = torch.device("cuda", torch.cuda.current_device())
-    bufs = []
-    for rep in (healthy, reduced):
-        for ga, gb in zip(rep.grad_a, rep.grad_b):
-            u = np.concatenate([np.asarray(ga).T, np.asarray(gb)], axis=1)
-            bufs.append(torch.from_numpy(np.ascontiguousarray(u, dtype=np.float64))
-                        .pin_memory().to(dev, non_blocking=True))
-    plan = build_pair_plan(healthy.cols, reduced.cols, smap.k, 2 * h, _lib.NTP_F64)
-    plan.finalize().upload(dev.index)
-    plan.grad_sync(tensor_ptrs(bufs), code, w_h, w_r)
-    outs = [b.cpu().numpy() for b in bufs]
-    i = 0
-    for rep in (healthy, reduced):
-        for ga, gb in zip(rep.grad_a, rep.grad_b):
-            ga[...] = outs[i][:, :h].T
-            gb[...] = outs[i][:, h:]
-            i += 1
+    key = (tuple(c.tobytes() for c in healthy.cols), tuple(c.tobytes() for c in reduced.cols),
+           healthy.layer.hidden, smap.k, dev.index)
+    path = _HOST_PATHS.get(key)
+    if path is None:
+        if len(_HOST_PATHS) > 16:
+            _HOST_PATHS.clear()
+        path = _HOST_PATHS[key] = _HostPath(healthy, reduced, smap.k, dev)
+    path.run(healthy, reduced, code, w_h, w_r)
 
 
 def uniform_grad_sync(replicas, op: str = "sum", weights=None) -> None:
@@ -371,6 +516,74 @@ def multi_grad_sync(replicas, op: str = "sum", weights=None) -> None:
 # attention gradients; here a head's four blocks (wq, wk, wv: [hidden x hd],
 # wo: [hd x hidden]) form one contiguous unit of 4*hidden*hd elements
 # (perfmodel.py:270-272) and heads sync exactly like MLP columns.
+
+
+@dataclass(frozen=True)
+class AttentionLayer:
+    """Multi-head attention weights (tpnumerics.py:70-112): wq/wk/wv
+    [H, hidden, head_dim], wo [H, head_dim, hidden], float64."""
+
+    wq: np.ndarray
+    wk: np.ndarray
+    wv: np.ndarray
+    wo: np.ndarray
+
+    def __post_init__(self):
+        for name in ("wq", "wk", "wv", "wo"):
+            object.__setattr__(self, name, np.asarray(getattr(self, name), dtype=np.float64))
+        if not (self.wq.shape == self.wk.shape == self.wv.shape):
+            raise ValueError("wq/wk/wv shapes differ")
+        H, hidden, head_dim = self.wq.shape
+        if self.wo.shape != (H, head_dim, hidden):
+            raise ValueError(f"wo shape {self.wo.shape} != {(H, head_dim, hidden)}")
+
+    @property
+    def heads(self) -> int:
+        return self.wq.shape[0]
+
+    @property
+    def hidden(self) -> int:
+        return self.wq.shape[1]
+
+    @property
+    def head_dim(self) -> int:
+        return self.wq.shape[2]
+
+    @classmethod
+    def random(cls, heads: int, hidden: int, head_dim: int, seed: int = 0) -> "AttentionLayer":
+        """Seeded N(0,1) draws in the reference's order: wq, wk, wv, wo."""
+        rng = np.random.default_rng(seed)
+        shapes = [(heads, hidden, head_dim)] * 3 + [(heads, head_dim, hidden)]
+        return cls(*(rng.standard_normal(s) for s in shapes))
+
+
+def _heads_output(X: torch.Tensor, layer: AttentionLayer, heads) -> torch.Tensor:
+    """sum over `heads` of softmax(Q K^T / sqrt(d)) V W_o (tpnumerics.py:188-199),
+    all heads of the set batched, float64."""
+    idx = torch.as_tensor(np.asarray(heads, dtype=np.int64), device=X.device)
+    wq, wk, wv, wo = (_dev64(w, X.device)[idx] for w in (layer.wq, layer.wk, layer.wv, layer.wo))
+    Q, K, V = (torch.einsum("th,nhd->ntd", X, w) for w in (wq, wk, wv))
+    P = torch.softmax(Q @ K.transpose(1, 2) / np.sqrt(layer.head_dim), dim=-1)
+    out = torch.zeros((X.shape[0], layer.hidden), dtype=torch.float64, device=X.device)
+    for o in torch.bmm(P @ V, wo):  # ascending head order, as the reference
+        out += o
+    return out
+
+
+def attention_forward_dense(X, layer: AttentionLayer):
+    """Sum of every head's output (tpnumerics.py:202-207), float64."""
+    return _out(_heads_output(_dev64(X), layer, np.arange(layer.heads)), X)
+
+
+def attention_forward_tp(X, replica):
+    """Per-rank partial sums over owned heads, ranks in ascending order
+    (tpnumerics.py:210-217), float64."""
+    Xd = _dev64(X)
+    Z = torch.zeros((Xd.shape[0], replica.layer.hidden), dtype=torch.float64, device=Xd.device)
+    for owned in replica.heads:
+        if len(owned):
+            Z += _heads_output(Xd, replica.layer, owned)
+    return _out(Z, X)
 
 
 class AttentionReplica:

@@ -5,7 +5,10 @@ all arenas and compares them with the oracle's fp64 nonuniform sync.
     torchrun --nproc-per-node N scripts/dist_check.py [n1 n2 dtype steps [launch [policy]]]
 
 launch: "fused" (default here, one ntp_grad_sync_step per step), "three" (post
-ready / signalled sync / wait done; NtpSyncGroup's default) or "alternate"; policy: the executor policy
+ready / signalled sync / wait done; NtpSyncGroup's default), "alternate", or
+"nccl" (n1 == n2: the aligned NCCL all-reduce fall-through), "graph" / "graph_fused"
+(CUDA-graph steps interleaved with eager ones) or "graph_multi" (every step in
+one graph); policy: the executor policy
 ("split" default, "healthy": the reduced side computes nothing and only
 hand-shakes)
 """
@@ -42,7 +45,10 @@ def main():
     lay = pair_layout(shape, n1, n2)
     plc = Placement.default(world, n1, n2)
     dtype = DT[dname]
-    grp = NtpSyncGroup(lay, plc, dtype, device=local, policy=policy).upload()
+    grp = NtpSyncGroup(lay, plc, dtype, device=local, policy=policy,
+                       aligned="nccl" if launch == "nccl" else "peer").upload()
+    if launch == "nccl":
+        assert grp.aligned == ("nccl" if n1 == n2 else "peer")
     rng = np.random.default_rng(0)
     init = [rng.standard_normal(e) for e in list(lay.h_elems) + list(lay.r_elems)]
     init = [torch.from_numpy(a).to(dtype).double().numpy() for a in init]  # representable
@@ -51,9 +57,14 @@ def main():
     torch.cuda.synchronize()
     dist.barrier()
     w = (4 / 7, 3 / 7)
-    for i in range(steps):
-        grp.fused_step = launch == "fused" or (launch == "alternate" and i % 2 == 0)
-        grp.step(*w)
+    if launch == "graph_multi":  # all steps recorded into one CUDA graph
+        grp.step_graph(*w, steps=steps)
+    for i in range(steps if launch != "graph_multi" else 0):
+        grp.fused_step = launch in ("fused", "graph_fused") or (launch == "alternate" and i % 2 == 0)
+        if launch.startswith("graph") and i % 2 == 0:
+            grp.step_graph(*w)  # graph replays interleaved with eager steps
+        else:
+            grp.step(*w)
     torch.cuda.synchronize()
     dist.barrier()
     assert grp.status() == 0, "signal timeout"

@@ -75,3 +75,46 @@ def test_verify_tp_numerics_on_device(capsys):
     rc, out, _ = run_cli(capsys, "verify", "--suite", "tp-numerics")
     assert rc == 0, out
     assert out.startswith("PASS tp-numerics")
+
+
+@pytest.mark.gpu
+def test_verify_all_four_suites(capsys):
+    """`verify` with no suite runs the reference's four suites (cli.py:320-325)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    rc, out, _ = run_cli(capsys, "verify")
+    assert rc == 0, out
+    assert [l.split(":")[0] for l in out.splitlines() if l.startswith("PASS")] == [
+        "PASS shard-invariants", "PASS tp-numerics", "PASS grad-finite-diff", "PASS golden"]
+    assert not any(l.startswith("FAIL") for l in out.splitlines())
+
+
+@pytest.mark.gpu
+def test_verify_golden_json(capsys):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    rc, out, _ = run_cli(capsys, "verify", "--suite", "golden", "--json")
+    doc = json.loads(out)
+    assert rc == 0 and doc["passed"] is True and doc["suites"][0]["name"] == "golden"
+
+
+@pytest.mark.gpu
+def test_verify_golden_catches_activation_drift(capsys, monkeypatch):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2504_06095_b200.tpnumerics as tpn
+    monkeypatch.setattr(tpn, "GELU_C", 0.0447)
+    rc, out, _ = run_cli(capsys, "verify", "--suite", "golden")
+    assert rc == 1 and "FAIL golden" in out and "case:" in out
+
+
+def test_golden_fixture_shipped_with_package():
+    """The package carries the reference's golden fixture (verify --suite golden)."""
+    from paper_2504_06095_b200.cli import _golden_fixture
+    with open(f"{ROOT}/tests/golden/golden_mlp.json") as f:
+        assert _golden_fixture() == json.load(f)
+
+
+def test_verify_suite_names():
+    from paper_2504_06095_b200.cli import SUITES
+    assert list(SUITES) == ["shard-invariants", "tp-numerics", "grad-finite-diff", "golden"]

@@ -41,6 +41,23 @@ def test_two_gpus_step_launch_variants(launch, policy):
     _run(2, 4, 3, "f32", 4, launch, policy)
 
 
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("n1", [4, 2])
+def test_two_gpus_aligned_nccl_fallthrough(n1, dtype):
+    """n1 == n2: shards line up, and NtpSyncGroup(aligned="nccl") syncs each
+    rank pair with a weighted NCCL all-reduce; same result as the oracle."""
+    _run(2, n1, n1, dtype, 2, "nccl")
+
+
+@pytest.mark.parametrize("launch,policy", [("graph", "split"), ("graph_fused", "split"),
+                                           ("graph_multi", "split"), ("graph", "healthy")])
+def test_two_gpus_cuda_graph_steps(launch, policy):
+    """Steps recorded into CUDA graphs with device-resident epochs (the *_dev
+    entry points), alone or interleaved with eager steps: same result as the
+    oracle after 5 steps."""
+    _run(2, 4, 3, "f32", 5, launch, policy)
+
+
 def test_four_gpus_tp2_tp1():
     _run(4, 2, 1, "f32", 2)
 
