@@ -181,6 +181,12 @@ int ntp_reshard(const ntp_plan *plan, void *const *bufs, int n_bufs, void *strea
 int ntp_uniform_sync(void *const *reps, int R, int64_t n, int dtype, int op, const double *w,
                      void *stream);
 
+/* dst = srcs[0] + srcs[1] + ... + srcs[R-1] in that order (accumulated in
+ * fp32, fp64 for f64), n elements; dst may alias one of the sources.  The
+ * owner's step of the row-parallel all-reduce (mlp_forward_tp's ascending-
+ * rank sum, tpnumerics.py:177-185, across GPUs: dist_linear.py). */
+int ntp_reduce_into(void *const *srcs, int R, int64_t n, int dtype, void *dst, void *stream);
+
 /* ------------------------------------------------------------------------
  * R-way sync for DP > 2 (no reference function: composes nonuniform_grad_sync,
  * tpnumerics.py:289-356, with uniform_grad_sync, 263-286)

@@ -564,7 +564,7 @@ __device__ __forceinline__ typename Acc<T>::type uniform_elem(const BufTable &re
 // unaligned buffers take the scalar path.
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
-uniform_kernel(BufTable reps, int R, int64_t n, int op, RepWeights w, int64_t n_vec) {
+uniform_kernel(BufTable reps, int R, int64_t n, int op, RepWeights w, int64_t n_vec, char *dst) {
   using A = typename Acc<T>::type;
   constexpr int kPer = 16 / sizeof(T);
   const int64_t stride = (int64_t)gridDim.x * kThreads;
@@ -595,11 +595,19 @@ uniform_kernel(BufTable reps, int R, int64_t n, int op, RepWeights w, int64_t n_
     T *oe = reinterpret_cast<T *>(&o);
 #pragma unroll
     for (int j = 0; j < kPer; ++j) oe[j] = T(op == NTP_OP_MEAN ? acc[j] / A(R) : acc[j]);
-    for (int r = 0; r < R; ++r) st_stream(reinterpret_cast<uint4 *>(reps.p[r]) + v, o);
+    if (dst) {
+      st_stream(reinterpret_cast<uint4 *>(dst) + v, o);
+    } else {
+      for (int r = 0; r < R; ++r) st_stream(reinterpret_cast<uint4 *>(reps.p[r]) + v, o);
+    }
   }
   for (int64_t e = n_vec * kPer + tid; e < n; e += stride) {
     const T o = T(uniform_elem<T>(reps, R, op, w, e));
-    for (int r = 0; r < R; ++r) reinterpret_cast<T *>(reps.p[r])[e] = o;
+    if (dst) {
+      reinterpret_cast<T *>(dst)[e] = o;
+    } else {
+      for (int r = 0; r < R; ++r) reinterpret_cast<T *>(reps.p[r])[e] = o;
+    }
   }
 }
 
@@ -753,6 +761,11 @@ static int set_device(int device) {
 // whatever the caller's current device is.
 static int set_device_of(cudaStream_t s) {
   if (!s) return NTP_OK;  // legacy default stream: the current device's
+  // cudaStreamGetDevice is not permitted on a capturing stream; a capture
+  // records the launch onto the stream's own graph whatever the current device
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  NTP_CUDA(cudaStreamIsCapturing(s, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return NTP_OK;
   int dev = -1;
   NTP_CUDA(cudaStreamGetDevice(s, &dev));
   return set_device(dev);
@@ -855,17 +868,17 @@ int ntp_reshard(const ntp_plan *p, void *const *bufs, int n_bufs, void *stream) 
   return NTP_OK;
 }
 
-int ntp_uniform_sync(void *const *reps, int R, int64_t n, int dtype, int op, const double *w,
-                     void *stream) {
+static int uniform_reduce(void *const *reps, int R, int64_t n, int dtype, int op,
+                          const double *w, void *dst, void *stream) {
   if (R < 1 || R > kMaxBufs) return fail(NTP_EINVAL, "replica count must be in [1, 64]");
   if (op < NTP_OP_SUM || op > NTP_OP_WEIGHTED) return fail(NTP_EINVAL, "unknown reduction op");
   if (n <= 0) return NTP_OK;
   cudaPointerAttributes attr{};
-  NTP_CUDA(cudaPointerGetAttributes(&attr, reps[0]));
+  NTP_CUDA(cudaPointerGetAttributes(&attr, dst ? dst : reps[0]));
   int st = set_device(attr.device);
   if (st) return st;
   BufTable bt{};
-  bool aligned = true;
+  bool aligned = !dst || (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;
   for (int r = 0; r < R; ++r) {
     bt.p[r] = static_cast<char *>(reps[r]);
     aligned &= (reinterpret_cast<uintptr_t>(reps[r]) & 15u) == 0;
@@ -881,15 +894,26 @@ int ntp_uniform_sync(void *const *reps, int R, int64_t n, int dtype, int op, con
   const int64_t work = n_vec + (n - n_vec * 16 / esize);
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((work + kThreads - 1) / kThreads,
                                                                  sm_count(attr.device) * 8));
+  char *d = static_cast<char *>(dst);
   switch (dtype) {
-    case NTP_F32: uniform_kernel<float><<<blocks, kThreads, 0, s>>>(bt, R, n, op, wv, n_vec); break;
-    case NTP_BF16: uniform_kernel<__nv_bfloat16><<<blocks, kThreads, 0, s>>>(bt, R, n, op, wv, n_vec); break;
-    case NTP_F16: uniform_kernel<__half><<<blocks, kThreads, 0, s>>>(bt, R, n, op, wv, n_vec); break;
-    case NTP_F64: uniform_kernel<double><<<blocks, kThreads, 0, s>>>(bt, R, n, op, wv, n_vec); break;
+    case NTP_F32: uniform_kernel<float><<<blocks, kThreads, 0, s>>>(bt, R, n, op, wv, n_vec, d); break;
+    case NTP_BF16: uniform_kernel<__nv_bfloat16><<<blocks, kThreads, 0, s>>>(bt, R, n, op, wv, n_vec, d); break;
+    case NTP_F16: uniform_kernel<__half><<<blocks, kThreads, 0, s>>>(bt, R, n, op, wv, n_vec, d); break;
+    case NTP_F64: uniform_kernel<double><<<blocks, kThreads, 0, s>>>(bt, R, n, op, wv, n_vec, d); break;
     default: return fail(NTP_EINVAL, "unsupported dtype");
   }
   NTP_CUDA(cudaGetLastError());
   return NTP_OK;
+}
+
+int ntp_uniform_sync(void *const *reps, int R, int64_t n, int dtype, int op, const double *w,
+                     void *stream) {
+  return uniform_reduce(reps, R, n, dtype, op, w, nullptr, stream);
+}
+
+int ntp_reduce_into(void *const *srcs, int R, int64_t n, int dtype, void *dst, void *stream) {
+  if (!dst) return fail(NTP_EINVAL, "dst is required");
+  return uniform_reduce(srcs, R, n, dtype, NTP_OP_SUM, nullptr, dst, stream);
 }
 
 // --------------------------------------------------------------------------

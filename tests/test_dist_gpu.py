@@ -107,6 +107,17 @@ def test_fused_wgrad_sync_multi_gpu(n, n1, n2, mode):
     _run_script(n, "fused_check.py", n1, n2, mode)
 
 
+@pytest.mark.parametrize("n,mode,layout,tokens", [(2, "push", "sync", 512), (2, "push", "comp", 500),
+                                                  (2, "nccl", "sync", 512), (4, "push", "sync", 1000),
+                                                  (4, "push", "comp", 512)])
+def test_row_parallel_forward_multi_gpu(n, mode, layout, tokens):
+    """dist_linear.TpMlpForward: column-parallel GEMM + row-parallel GEMM whose
+    epilogue pushes partial-sum boxes to the row-block owners over NVLink,
+    owner sums in rank order, peer gather; vs the fp64 oracle (<= 2e-2) and
+    bit-identical on every rank."""
+    _run_script(n, "tp_forward_check.py", mode, layout, tokens)
+
+
 @pytest.mark.parametrize("n,n1,dead", [(1, 4, 3), (2, 4, 1), (4, 2, 0)])
 def test_failure_reconfig_multi_gpu(n, n1, dead):
     """dist_reconfig: H -> comp layout, D's survivors -> TP-(n1-1), the dead
