@@ -44,9 +44,17 @@ def main():
         out["per_gpu_direction_bytes"] = g
         busiest = max(g.values())
         out["busiest_direction_bytes"] = busiest
+        if "nvltx__bytes_data_user.sum" in k0:
+            u = {"gpu0_tx": k0["nvltx__bytes_data_user.sum"] + k1["nvlrx__bytes_data_user.sum"],
+                 "gpu0_rx": k0["nvlrx__bytes_data_user.sum"] + k1["nvltx__bytes_data_user.sum"]}
+            out["per_gpu_direction_user_data_bytes"] = u
+            out["busiest_direction_user_data_bytes"] = max(u.values())
         if algo:
             out["algorithmic_bytes"] = algo
             out["busiest_over_algorithmic"] = round(busiest / algo, 4)
+            if "busiest_direction_user_data_bytes" in out:
+                out["user_data_over_algorithmic"] = round(
+                    out["busiest_direction_user_data_bytes"] / algo, 4)
     print(json.dumps(out, indent=1))
 
 
