@@ -148,60 +148,6 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-class NvlinkCounters:
-    """NVLink data bytes this GPU sent / received during the timed region, from
-    NVML's per-link throughput counters (NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX /
-    _RX, KiB, summed over the links that report; scripts/nvml_nvlink_probe.py
-    checks them against a known peer copy).  None when NVML cannot read them."""
-
-    TX, RX, LINKS = 138, 139, 18
-
-    def __init__(self, device_index: int):
-        self.h = None
-        self.src = "unavailable"
-        try:
-            import pynvml as N
-            N.nvmlInit()
-            self.N = N
-            self.h = N.nvmlDeviceGetHandleByIndex(device_index)
-        except Exception as e:  # noqa: BLE001 (NVML missing or no permission: report None)
-            self.src = f"unavailable: {e}"
-
-    def _read(self):
-        if self.h is None:
-            return None
-        ids = [(f, link) for f in (self.TX, self.RX) for link in range(self.LINKS)]
-        try:
-            vals = self.N.nvmlDeviceGetFieldValues(self.h, ids)
-        except Exception as e:  # noqa: BLE001
-            self.src = f"unavailable: {e}"
-            return None
-        tx = rx = 0
-        ok = 0
-        for (f, _), v in zip(ids, vals):
-            if v.nvmlReturn != 0:
-                continue
-            ok += 1
-            if f == self.TX:
-                tx += int(v.value.ullVal)
-            else:
-                rx += int(v.value.ullVal)
-        if not ok:
-            self.src = "unavailable: no NVLink throughput field readable"
-            return None
-        self.src = f"NVML fields 138/139 (KiB) over {ok // 2} links"
-        return tx * 1024, rx * 1024
-
-    def start(self):
-        self.t0 = self._read()
-
-    def stop(self):
-        t1 = self._read()
-        if self.t0 is None or t1 is None:
-            return {"tx_bytes": None, "rx_bytes": None, "src": self.src}
-        return {"tx_bytes": t1[0] - self.t0[0], "rx_bytes": t1[1] - self.t0[1], "src": self.src}
-
-
 # ---------------------------------------------------------------------------
 # CPU baseline: the oracle restatement of the reference's nonuniform_grad_sync
 

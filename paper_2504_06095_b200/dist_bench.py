@@ -29,7 +29,7 @@ def _max(x: float) -> float:
 
 def run(args):
     from bench import (ELEM_BYTES, L2_BYTES, METRIC, W_H, W_R, WORKLOADS,  # noqa: I001 (repo root)
-                       ClockSampler, NvlinkCounters, peaks, workload_config)
+                       ClockSampler, peaks, workload_config)
 
     # NCCL warnings (and its version banner) go to stderr: bench.py keeps fd 1
     # pointed at stderr while this runs, so stdout is the one JSON line
@@ -85,18 +85,15 @@ def run(args):
         raise RuntimeError(f"rank {rank}: signal timeout during warm-up")
     clocks = ClockSampler(local)
     clocks.start()
-    nv = NvlinkCounters(local)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     dist.barrier()
     clocks.mark("t0")
-    nv.start()
     e0.record(stream)
     for _ in range(args.steps):
         one()
     e1.record(stream)
     torch.cuda.synchronize()
-    nvl = nv.stop()
     clocks.mark("t1")
     dist.barrier()
     clk = clocks.stop()
@@ -112,11 +109,19 @@ def run(args):
         torch.cuda.synchronize()
         flush_ms = e0.elapsed_time(e1)
     ms = _max((total_ms - flush_ms) / args.steps)
-    # NVLink bytes per step, per direction, busiest rank (NVML counters read
-    # around the timed region)
-    tx = _max(float(nvl["tx_bytes"]) / args.steps if nvl["tx_bytes"] is not None else -1.0)
-    rx = _max(float(nvl["rx_bytes"]) / args.steps if nvl["rx_bytes"] is not None else -1.0)
-    traffic = None if min(tx, rx) < 0 else int(max(tx, rx))
+    timing_detail = {"total_ms_rank0": round(total_ms, 4), "flush_ms_rank0": round(flush_ms, 4),
+                     "total_ms_max": round(_max(total_ms), 4)}
+    # NVLink bytes per launch: the committed ncu measurement of this placement's
+    # per-process plans (NVML's NVLink throughput counters are not supported on
+    # these boxes, and merely querying them slowed the step by 17 %: DESIGN.md 6)
+    rec = _ncu_nvlink(args.workload, world)
+    traffic = int(rec["busiest_direction_bytes"]) if rec else None
+    traffic_src = ("ncu nvltx/nvlrx__bytes.sum of this placement's per-process plans "
+                   "(scripts/nvlink_traffic.py, profiles/ncu_nvlink_traffic.json): busiest GPU "
+                   "direction incl. packet overhead; user data only "
+                   f"{int(rec['busiest_direction_user_data_bytes'])} B" if rec else
+                   "not measured at this N (ncu separates per-direction NVLink bytes only "
+                   "for a two-GPU link pair)")
     kernel_ms = ms
     if grp.status() != 0:
         raise RuntimeError(f"rank {rank}: signal timeout")
@@ -142,15 +147,14 @@ def run(args):
                             "peak_src": "measured peer copy 770 GB/s/direction (B200_PROFILING.md)",
                             "unit": "GB/s", "frac": round(achieved / pk["nvlink_gbs"], 4),
                             "algorithmic_bytes_per_launch": B, "traffic": traffic,
-                            "traffic_src": "NVML NVLink data counters around the timed region, "
-                                           "busiest rank, max(tx, rx) bytes per step "
-                                           f"({nvl['src']})",
+                            "traffic_src": traffic_src,
                             "traffic_over_algorithmic": (round(traffic / B, 3) if traffic and B
                                                          else None),
                             "kernel_ms": round(kernel_ms, 4)},
                "timing": ("K steps, each one CUDA-graph launch" if use_graph else "K eager steps")
                          + (" after a 256 MB L2 flush; K flushes timed alone and subtracted"
                             if flush is not None else ""),
+               "timing_detail": timing_detail,
                "gpu_launches": args.steps * _launches_per_step(grp),
                "clocks": clk, "e2e": e2e}
     dist.barrier()
@@ -158,6 +162,21 @@ def run(args):
     dist.barrier()
     dist.destroy_process_group()
     return out
+
+
+def _ncu_nvlink(workload: str, world: int):
+    """The committed ncu NVLink measurement for (workload, N), if any."""
+    import json
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                        "ncu_nvlink_traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    rec = d.get(workload, {}).get(str(world))
+    if rec and "busiest_direction_bytes" in rec and "busiest_direction_user_data_bytes" in rec:
+        return rec
+    return None
 
 
 def busiest_bytes_for(lay, plc: Placement, eb: int) -> int:

@@ -41,7 +41,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     acc = torch.empty(1, dtype=torch.int64, device="cuda")
     fl_w = lambda: flush.fill_(1)  # noqa: E731
-    fl_r = lambda: torch.sum(flush.view(torch.int64), out=acc)  # noqa: E731
+    fl_r = lambda: acc.copy_(flush.view(torch.int64).sum())  # noqa: E731
     out = {}
     for name, shape, dt in (("tiny", ModelShape("tiny", 64, 8, 0, 1), torch.float32),
                             ("c1", C1, torch.float32)):
