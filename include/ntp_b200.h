@@ -181,11 +181,14 @@ int ntp_reshard(const ntp_plan *plan, void *const *bufs, int n_bufs, void *strea
 int ntp_uniform_sync(void *const *reps, int R, int64_t n, int dtype, int op, const double *w,
                      void *stream);
 
-/* dst = srcs[0] + srcs[1] + ... + srcs[R-1] in that order (accumulated in
- * fp32, fp64 for f64), n elements; dst may alias one of the sources.  The
- * owner's step of the row-parallel all-reduce (mlp_forward_tp's ascending-
- * rank sum, tpnumerics.py:177-185, across GPUs: dist_linear.py). */
-int ntp_reduce_into(void *const *srcs, int R, int64_t n, int dtype, void *dst, void *stream);
+/* dsts[d] = srcs[0] + srcs[1] + ... + srcs[R-1] in that order (accumulated in
+ * fp32, fp64 for f64) for every d < n_dst, n elements; a destination may alias
+ * a source and may be a peer GPU's (IPC-mapped) memory.  The owner's step of
+ * the row-parallel all-reduce (mlp_forward_tp's ascending-rank sum,
+ * tpnumerics.py:177-185, across GPUs: dist_linear.py): sum the pushed partial
+ * sums and write the block into every rank's output at once. */
+int ntp_reduce_into(void *const *srcs, int R, int64_t n, int dtype, void *const *dsts, int n_dst,
+                    void *stream);
 
 /* ------------------------------------------------------------------------
  * R-way sync for DP > 2 (no reference function: composes nonuniform_grad_sync,

@@ -66,8 +66,8 @@ SIGNATURES = {
     "ntp_reshard": (ctypes.c_int, [_vp, _vpp, ctypes.c_int, _vp]),
     "ntp_uniform_sync": (ctypes.c_int, [_vpp, ctypes.c_int, ctypes.c_int64, ctypes.c_int,
                                         ctypes.c_int, ctypes.POINTER(ctypes.c_double), _vp]),
-    "ntp_reduce_into": (ctypes.c_int, [_vpp, ctypes.c_int, ctypes.c_int64, ctypes.c_int, _vp,
-                                       _vp]),
+    "ntp_reduce_into": (ctypes.c_int, [_vpp, ctypes.c_int, ctypes.c_int64, ctypes.c_int, _vpp,
+                                       ctypes.c_int, _vp]),
     "ntp_mplan_create": (ctypes.c_int, [ctypes.POINTER(_vp), ctypes.c_int, ctypes.c_int]),
     "ntp_mplan_add_units": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, _i32p, _i64p]),
     "ntp_mplan_finalize": (ctypes.c_int, [_vp]),

@@ -564,7 +564,8 @@ __device__ __forceinline__ typename Acc<T>::type uniform_elem(const BufTable &re
 // unaligned buffers take the scalar path.
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
-uniform_kernel(BufTable reps, int R, int64_t n, int op, RepWeights w, int64_t n_vec, char *dst) {
+uniform_kernel(BufTable reps, int R, int64_t n, int op, RepWeights w, int64_t n_vec, BufTable dst,
+               int n_dst) {
   using A = typename Acc<T>::type;
   constexpr int kPer = 16 / sizeof(T);
   const int64_t stride = (int64_t)gridDim.x * kThreads;
@@ -595,16 +596,16 @@ uniform_kernel(BufTable reps, int R, int64_t n, int op, RepWeights w, int64_t n_
     T *oe = reinterpret_cast<T *>(&o);
 #pragma unroll
     for (int j = 0; j < kPer; ++j) oe[j] = T(op == NTP_OP_MEAN ? acc[j] / A(R) : acc[j]);
-    if (dst) {
-      st_stream(reinterpret_cast<uint4 *>(dst) + v, o);
+    if (n_dst) {
+      for (int d = 0; d < n_dst; ++d) st_stream(reinterpret_cast<uint4 *>(dst.p[d]) + v, o);
     } else {
       for (int r = 0; r < R; ++r) st_stream(reinterpret_cast<uint4 *>(reps.p[r]) + v, o);
     }
   }
   for (int64_t e = n_vec * kPer + tid; e < n; e += stride) {
     const T o = T(uniform_elem<T>(reps, R, op, w, e));
-    if (dst) {
-      reinterpret_cast<T *>(dst)[e] = o;
+    if (n_dst) {
+      for (int d = 0; d < n_dst; ++d) reinterpret_cast<T *>(dst.p[d])[e] = o;
     } else {
       for (int r = 0; r < R; ++r) reinterpret_cast<T *>(reps.p[r])[e] = o;
     }
@@ -869,16 +870,22 @@ int ntp_reshard(const ntp_plan *p, void *const *bufs, int n_bufs, void *stream) 
 }
 
 static int uniform_reduce(void *const *reps, int R, int64_t n, int dtype, int op,
-                          const double *w, void *dst, void *stream) {
+                          const double *w, void *const *dsts, int n_dst, void *stream) {
   if (R < 1 || R > kMaxBufs) return fail(NTP_EINVAL, "replica count must be in [1, 64]");
+  if (n_dst < 0 || n_dst > kMaxBufs) return fail(NTP_EINVAL, "destination count must be in [0, 64]");
   if (op < NTP_OP_SUM || op > NTP_OP_WEIGHTED) return fail(NTP_EINVAL, "unknown reduction op");
   if (n <= 0) return NTP_OK;
   cudaPointerAttributes attr{};
-  NTP_CUDA(cudaPointerGetAttributes(&attr, dst ? dst : reps[0]));
+  NTP_CUDA(cudaPointerGetAttributes(&attr, reps[0]));
   int st = set_device(attr.device);
   if (st) return st;
-  BufTable bt{};
-  bool aligned = !dst || (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;
+  BufTable bt{}, dt{};
+  bool aligned = true;
+  for (int d = 0; d < n_dst; ++d) {
+    if (!dsts[d]) return fail(NTP_EINVAL, "null destination");
+    dt.p[d] = static_cast<char *>(dsts[d]);
+    aligned &= (reinterpret_cast<uintptr_t>(dsts[d]) & 15u) == 0;
+  }
   for (int r = 0; r < R; ++r) {
     bt.p[r] = static_cast<char *>(reps[r]);
     aligned &= (reinterpret_cast<uintptr_t>(reps[r]) & 15u) == 0;
@@ -894,12 +901,11 @@ static int uniform_reduce(void *const *reps, int R, int64_t n, int dtype, int op
   const int64_t work = n_vec + (n - n_vec * 16 / esize);
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((work + kThreads - 1) / kThreads,
                                                                  sm_count(attr.device) * 8));
-  char *d = static_cast<char *>(dst);
   switch (dtype) {
-    case NTP_F32: uniform_kernel<float><<<blocks, kThreads, 0, s>>>(bt, R, n, op, wv, n_vec, d); break;
-    case NTP_BF16: uniform_kernel<__nv_bfloat16><<<blocks, kThreads, 0, s>>>(bt, R, n, op, wv, n_vec, d); break;
-    case NTP_F16: uniform_kernel<__half><<<blocks, kThreads, 0, s>>>(bt, R, n, op, wv, n_vec, d); break;
-    case NTP_F64: uniform_kernel<double><<<blocks, kThreads, 0, s>>>(bt, R, n, op, wv, n_vec, d); break;
+    case NTP_F32: uniform_kernel<float><<<blocks, kThreads, 0, s>>>(bt, R, n, op, wv, n_vec, dt, n_dst); break;
+    case NTP_BF16: uniform_kernel<__nv_bfloat16><<<blocks, kThreads, 0, s>>>(bt, R, n, op, wv, n_vec, dt, n_dst); break;
+    case NTP_F16: uniform_kernel<__half><<<blocks, kThreads, 0, s>>>(bt, R, n, op, wv, n_vec, dt, n_dst); break;
+    case NTP_F64: uniform_kernel<double><<<blocks, kThreads, 0, s>>>(bt, R, n, op, wv, n_vec, dt, n_dst); break;
     default: return fail(NTP_EINVAL, "unsupported dtype");
   }
   NTP_CUDA(cudaGetLastError());
@@ -908,12 +914,13 @@ static int uniform_reduce(void *const *reps, int R, int64_t n, int dtype, int op
 
 int ntp_uniform_sync(void *const *reps, int R, int64_t n, int dtype, int op, const double *w,
                      void *stream) {
-  return uniform_reduce(reps, R, n, dtype, op, w, nullptr, stream);
+  return uniform_reduce(reps, R, n, dtype, op, w, nullptr, 0, stream);
 }
 
-int ntp_reduce_into(void *const *srcs, int R, int64_t n, int dtype, void *dst, void *stream) {
-  if (!dst) return fail(NTP_EINVAL, "dst is required");
-  return uniform_reduce(srcs, R, n, dtype, NTP_OP_SUM, nullptr, dst, stream);
+int ntp_reduce_into(void *const *srcs, int R, int64_t n, int dtype, void *const *dsts, int n_dst,
+                    void *stream) {
+  if (n_dst < 1) return fail(NTP_EINVAL, "at least one destination is required");
+  return uniform_reduce(srcs, R, n, dtype, NTP_OP_SUM, nullptr, dsts, n_dst, stream);
 }
 
 // --------------------------------------------------------------------------

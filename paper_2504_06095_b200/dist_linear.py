@@ -16,10 +16,11 @@ GPUs.  Mode "push" (default) does that all-reduce inside the second GEMM:
    box; ``ntp_gemm_bf16_red`` mode 2).  The reduce-scatter is therefore done
    tile by tile while the GEMM runs: no separate send.
 3. Once every rank has pushed (device signals, no host sync), the owner of
-   row block ``j`` sums slots 0..n-1 **in ascending rank order** into its
-   ``Z`` rows (``ntp_reduce_into``, fp32) -- the reference's summation order.
-4. Every rank copies the other row blocks of ``Z`` from their owners' HBM
-   (peer reads over NVLink): ``Z`` ends bit-identical on every rank.
+   row block ``j`` sums slots 0..n-1 **in ascending rank order** (fp32, the
+   reference's summation order) and writes the sum straight into the ``j``
+   rows of every rank's ``Z``: its own and, over NVLink, the peers'
+   (``ntp_reduce_into`` with n destinations).  ``Z`` ends bit-identical on
+   every rank after one more handshake; there is no separate gather.
 
 Mode "nccl" is the library baseline: the same two GEMMs with a plain local
 output, then ``torch.distributed.all_reduce`` (NCCL) of ``Z``.
@@ -97,12 +98,15 @@ class TpMlpForward:
         slot = self.rank * self.Tb * self.h * 4
         self.red_bases = [(self.peer_stg[j] + slot) if j != self.rank else (self._stg + slot)
                           for j in range(self.n)]
-        # owner reduce: slot r of the own staging, except slot `rank` = own Z rows
+        # owner reduce: slot r of the own staging, except slot `rank` = own Z rows;
+        # the sum goes to the own block's rows of every rank's Z (own first)
         lo, hi = self.blocks[self.rank]
         self._own_rows = (lo, hi)
         srcs = [self._z + lo * self.h * 4 if r == self.rank
                 else self._stg + r * self.Tb * self.h * 4 for r in range(self.n)]
         self._srcs = _lib.ptr_array(srcs)
+        dsts = [self._z + lo * self.h * 4] + [self.peer_z[j] + lo * self.h * 4 for j in self.peers]
+        self._dsts = _lib.ptr_array(dsts)
         # signal words: region g, writer w -> page + 8*(g*_WORDS + w)
         self._post = {g: _lib.u64_ptr_array([self.peer_sig[j] + 8 * (g * _WORDS + self.rank)
                                              for j in self.peers]) for g in range(3)}
@@ -148,22 +152,16 @@ class TpMlpForward:
                    self.red_bases, self.h, stream=s, mode="push_tma")
             self._signal(_PUSHED, "post", s)
             self._signal(_PUSHED, "wait", s)
-            # 3. own row block: slots 0..n-1 summed in rank order (slot rank = own Z rows)
+            # 3. own row block: slots 0..n-1 summed in rank order (slot rank = own Z
+            # rows), written into this block of every rank's Z (peer stores over NVLink)
             lo, hi = self._own_rows
             if hi > lo:
                 _lib.check(_lib.load().ntp_reduce_into(
                     self._srcs, self.n, (hi - lo) * self.h, dtype_code(torch.float32),
-                    ctypes.c_void_p(self._z + lo * self.h * 4), ctypes.c_void_p(s.cuda_stream)),
-                    "ntp_reduce_into")
+                    self._dsts, self.n, ctypes.c_void_p(s.cuda_stream)), "ntp_reduce_into")
+            # 4. every block has landed in this rank's Z
             self._signal(_REDUCED, "post", s)
             self._signal(_REDUCED, "wait", s)
-            # 4. the other row blocks from their owners (peer reads over NVLink)
-            for j in self.peers:
-                lo, hi = self.blocks[j]
-                if hi > lo:
-                    src = _wrap(self.peer_z[j] + lo * self.h * 4, (hi - lo) * self.h,
-                                torch.float32, self.device)
-                    self.Z[lo:hi].view(-1).copy_(src, non_blocking=True)
         return self.Z
 
     def status(self) -> int:
