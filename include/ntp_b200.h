@@ -167,6 +167,15 @@ int ntp_grad_sync(const ntp_plan *plan, void *const *bufs, int n_bufs, int op, d
 int ntp_grad_sync_ex(const ntp_plan *plan, void *const *bufs, int n_bufs, int op, double w_a,
                      double w_b, int write_mask, void *stream);
 
+/* Static memory-safety check of a finalized plan (no device work): every
+ * chunk's element range on both sides lies inside its buffer (buf_elems[b]
+ * elements, n_bufs buffers), and, for the sides in write_sides (bit 0: side
+ * A, bit 1: side B; 3 for a sync, 2 for a reshard copy), no element is written
+ * by two chunks, i.e. no two CTAs of a launch write the same bytes.  Returns
+ * NTP_EINVAL naming the offending chunk(s).  (compute-sanitizer is closed on
+ * the B200 pool: this, the canary tests and the oracle comparisons stand in.) */
+int ntp_plan_check(const ntp_plan *plan, const int64_t *buf_elems, int n_bufs, int write_sides);
+
 /* Reconfiguration copy (no reference function; built from build_reshard_plan
  * 185-206 / apply_plan 209-217 / contiguous_assignment tpnumerics.py:115-120):
  * B = A for every unit.  Bit-exact. */

@@ -57,6 +57,7 @@ SIGNATURES = {
     "ntp_plan_finalize": (ctypes.c_int, [_vp]),
     "ntp_plan_stats_get": (ctypes.c_int, [_vp, ctypes.POINTER(PlanStats)]),
     "ntp_plan_export": (ctypes.c_int, [_vp, _i64p]),
+    "ntp_plan_check": (ctypes.c_int, [_vp, _i64p, ctypes.c_int, ctypes.c_int]),
     "ntp_plan_upload": (ctypes.c_int, [_vp, ctypes.c_int]),
     "ntp_plan_destroy": (None, [_vp]),
     "ntp_grad_sync": (ctypes.c_int, [_vp, _vpp, ctypes.c_int, ctypes.c_int, ctypes.c_double,

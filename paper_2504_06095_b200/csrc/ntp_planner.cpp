@@ -298,6 +298,46 @@ int ntp_plan_export(const ntp_plan *p, int64_t *out) {
   return NTP_OK;
 }
 
+int ntp_plan_check(const ntp_plan *p, const int64_t *buf_elems, int n_bufs, int write_sides) {
+  if (!p || (!buf_elems && n_bufs)) return fail(NTP_EINVAL, "null argument");
+  if (!p->finalized) return fail(NTP_ESTATE, "plan not finalized");
+  if (write_sides < 0 || write_sides > 3) return fail(NTP_EINVAL, "write_sides must be 0..3");
+  const int64_t grain = p->vectorized ? 16 / dtype_bytes(p->dtype) : 1;
+  struct Range {
+    int64_t buf, lo, hi, chunk;
+  };
+  std::vector<Range> writes;
+  writes.reserve(2 * p->chunks.size());
+  for (size_t i = 0; i < p->chunks.size(); ++i) {
+    const Chunk &c = p->chunks[i];
+    const int64_t len = (int64_t)c.len * grain;
+    const int64_t side_buf[2] = {c.a_buf, c.b_buf};
+    const int64_t side_off[2] = {(int64_t)c.a_off * grain, (int64_t)c.b_off * grain};
+    for (int side = 0; side < 2; ++side) {
+      const int64_t b = side_buf[side], lo = side_off[side];
+      if (b >= n_bufs)
+        return fail(NTP_EINVAL, "chunk " + std::to_string(i) + " uses buffer " + std::to_string(b) +
+                                    " of " + std::to_string(n_bufs));
+      if (lo + len > buf_elems[b])
+        return fail(NTP_EINVAL, "chunk " + std::to_string(i) + ": buffer " + std::to_string(b) +
+                                    " elements [" + std::to_string(lo) + ", " +
+                                    std::to_string(lo + len) + ") exceed its " +
+                                    std::to_string(buf_elems[b]));
+      if (write_sides & (1 << side)) writes.push_back(Range{b, lo, lo + len, (int64_t)i});
+    }
+  }
+  // every element is written by one chunk at most: no two CTAs race on it
+  std::sort(writes.begin(), writes.end(), [](const Range &x, const Range &y) {
+    return x.buf != y.buf ? x.buf < y.buf : x.lo < y.lo;
+  });
+  for (size_t i = 1; i < writes.size(); ++i)
+    if (writes[i].buf == writes[i - 1].buf && writes[i].lo < writes[i - 1].hi)
+      return fail(NTP_EINVAL, "chunks " + std::to_string(writes[i - 1].chunk) + " and " +
+                                  std::to_string(writes[i].chunk) + " write overlapping elements of buffer " +
+                                  std::to_string(writes[i].buf));
+  return NTP_OK;
+}
+
 void ntp_plan_destroy(ntp_plan *p) {
   if (!p) return;
   if (p->d_chunks) device_free(p->d_chunks, p->device);

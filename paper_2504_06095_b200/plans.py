@@ -93,6 +93,16 @@ class Plan:
 
     # -- device execution ------------------------------------------------------
 
+    def check(self, buf_elems, write_sides: int = 3) -> "Plan":
+        """Static memory-safety check (ntp_plan_check): every chunk inside its
+        buffer (buf_elems[b] elements) and no element written twice on the
+        sides in write_sides (3: a sync, 2: a reshard copy).  ValueError names
+        the offending chunk."""
+        sizes = np.ascontiguousarray(buf_elems, dtype=np.int64)
+        _lib.check(self._L.ntp_plan_check(self._h, _lib.p64(sizes), len(sizes), int(write_sides)),
+                   "ntp_plan_check")
+        return self
+
     def grad_sync(self, bufs, op: int, w_a: float = 1.0, w_b: float = 1.0, stream=None) -> None:
         ptrs = _lib.ptr_array(bufs)
         _lib.check(self._L.ntp_grad_sync(self._h, ptrs, len(bufs), int(op), float(w_a),

@@ -1,7 +1,11 @@
-"""OverlappedBackward (paper_2504_06095_b200.step) on N GPUs under torchrun:
-the overlapped step (GEMMs on the main stream, each layer's sync on a side
-stream, healthy-executor policy, capped kernels) must give the same bits as
-the plain order -- all GEMMs, then every layer's sync (split policy).
+"""OverlappedBackward (paper_2504_06095_b200.step) on N GPUs under torchrun
+(N = 1 too: every logical rank on one GPU): the overlapped step (GEMMs on the
+main stream, each layer's sync on a side stream, healthy-executor policy,
+capped kernels) must give the same bits as the plain order -- all GEMMs, then
+every layer's sync (split policy) -- and match the fp64 oracle: per layer the
+dense w_h * mlp_backward(X_h) + w_r * mlp_backward(X_r) (tpnumerics.py:220-235
+summed as nonuniform_grad_sync does, 289-356) on the same bf16-rounded
+weights and activations, <= 2e-2, in both replicas' layouts.
 
     torchrun --nproc-per-node N scripts/step_check.py [n1 n2 layers]
 """
@@ -14,6 +18,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
+from oracle import oracle as O  # noqa: E402
 from paper_2504_06095_b200.dist import NtpSyncGroup, Placement  # noqa: E402
 from paper_2504_06095_b200.linear import MlpShard  # noqa: E402
 from paper_2504_06095_b200.step import OverlappedBackward  # noqa: E402
@@ -35,22 +40,23 @@ def main():
     tok_r = tok * n2 // n1
     w_h, w_r = tok / (tok + tok_r), tok_r / (tok + tok_r)
     _k, _u, hc, rc, _hb, _rb = lay.segs[0]
-    rng = np.random.default_rng(0)   # same weights everywhere
-    g = torch.Generator(device="cuda").manual_seed(1)
-    layers, inputs = [], []
+    rng = np.random.default_rng(0)   # same weights and activations on every rank
+    bf = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(torch.bfloat16)  # noqa: E731
+    layers, inputs, dense = [], [], []
     for li in range(L):
-        A = rng.standard_normal((h, k)) / np.sqrt(h)
-        B = rng.standard_normal((k, h)) / np.sqrt(k)
+        A = bf(rng.standard_normal((h, k)) / np.sqrt(h)).double().numpy()
+        B = bf(rng.standard_normal((k, h)) / np.sqrt(k)).double().numpy()
+        XG = {side: [bf(rng.standard_normal((T, h))) for _ in range(2)]
+              for side, T in (("h", tok), ("r", tok_r))}
+        dense.append((A, B, {sd: [t.double().numpy() for t in v] for sd, v in XG.items()}))
         grp = NtpSyncGroup(lay, plc, torch.float32, local).upload()
         shards, ins = [], []
         for s in grp.hosted:
             healthy = s < n1
             cols = hc[s] if healthy else rc[s - n1]
             sh = MlpShard(A, B, cols)
-            T = tok if healthy else tok_r
-            X = torch.randn((T, h), generator=g, device="cuda").to(torch.bfloat16)
-            G = torch.randn((T, h), generator=g, device="cuda").to(torch.bfloat16)
-            sh.forward(X, torch.empty((T, h), dtype=torch.float32, device="cuda"))
+            X, G = (t.cuda() for t in XG["h" if healthy else "r"])
+            sh.activations(X)
             shards.append((sh, grp.arena(s).view(len(cols), 2, h)))
             ins.append((X, G))
         layers.append((grp, shards))
@@ -79,6 +85,26 @@ def main():
             assert grp.status() == 0, "signal timeout"
             for (_sh, grads), ref in zip(shards, w):
                 ok &= bool(torch.equal(grads, ref))
+    # fp64 oracle: rank 0 gathers every hosted arena and checks each layer
+    mine = [{s: grads.double().cpu().numpy().reshape(grads.shape[0], -1)
+             for s, (_sh, grads) in zip(grp.hosted, shards)} for grp, shards in layers]
+    allv = [None] * world
+    dist.all_gather_object(allv, mine)
+    worst = 0.0
+    if rank == 0:
+        for li, (A, B, XG) in enumerate(dense):
+            got = {}
+            for d in allv:
+                got.update(d[li])
+            want_a, want_b = (w_h * a + w_r * b for a, b in
+                              zip(O.mlp_backward(*XG["h"][:1], A, B, XG["h"][1]),
+                                  O.mlp_backward(*XG["r"][:1], A, B, XG["r"][1])))
+            for side, cols in (("h", hc), ("r", rc)):
+                base = 0 if side == "h" else n1
+                da, db = O.dense_from_units([got[base + i] for i in range(len(cols))], cols, h, k)
+                worst = max(worst, O.rel_err(da, want_a), O.rel_err(db, want_b))
+        ok &= worst <= 2e-2
+        print(f"oracle worst rel err {worst:.3e}", flush=True)
     t = torch.tensor([int(ok)], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MIN)
     if rank == 0:
