@@ -210,6 +210,12 @@ struct Params {
   int epi_sleep;  // 1: the epilogue polls its accumulator barrier with a sleep
   int debug;      // experiments: 1 = no operand loads, 2 = no epilogue output,
                   // 4 = MMA skips the full-stage waits, 8 = no stage commits (no producer)
+  // TMA stores clip the inner dimension at 16-byte granularity, not per
+  // element (found by tests/test_bounds_gpu.py: with N*esize % 16 != 0 a box
+  // at the row end also wrote the bytes up to the next 16-byte boundary, i.e.
+  // into the pitch gap -- in a unit-major arena, the next half-unit).  Boxes
+  // that reach past tma_cols are stored element by element instead.
+  int tma_cols;
 };
 
 // tile t -> (M-tile, N-tile) under the grouped raster order
@@ -692,6 +698,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         // one peer copy, else row stores from registers (run boundaries, ragged M)
         int peer_box = -1, peer_row0 = 0;
         const bool reduce = kEpi == EPI_RED;  // only reached with tma_red
+        const bool tma_box = col0 + 32 <= p.tma_cols;
         if (kEpi == EPI_PUSH || reduce) {
           const int pb = row < p.M ? p.red_buf[row] : -1;
           const int pr = row < p.M ? p.red_row[row] : 0;
@@ -711,14 +718,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             tma_reduce_add_2d(&map_c, stage, col0, row0);
             if (peer_box >= 0) tma_reduce_add_2d(&peer_maps.m[peer_box], stage, col0, peer_row0);
           } else {
-            if (p.c_tma) tma_store_2d(&map_c, stage, col0, row0);  // TMA clips rows >= M, cols >= N
-            if (kEpi == EPI_GELU && p.h_tma) tma_store_2d(&map_h, stage + 2048, col0, row0);
+            // TMA clips rows >= M; columns only up to tma_cols (16-byte granules)
+            if (p.c_tma && tma_box) tma_store_2d(&map_c, stage, col0, row0);
+            if (kEpi == EPI_GELU && p.h_tma && tma_box)
+              tma_store_2d(&map_h, stage + 2048, col0, row0);
             if (peer_box >= 0) tma_store_2d(&peer_maps.m[peer_box], stage, col0, peer_row0);
           }
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
-        if (!p.c_tma) box_store(stage, p.C, p.ldc, p.c_f32 ? 4 : 2, row0, col0, p.M, p.N, lane);
-        if (kEpi == EPI_GELU && !p.h_tma)
+        if (!p.c_tma || !tma_box) box_store(stage, p.C, p.ldc, p.c_f32 ? 4 : 2, row0, col0, p.M, p.N, lane);
+        if (kEpi == EPI_GELU && (!p.h_tma || !tma_box))
           box_store(stage + 2048, p.H, p.ldh, 2, row0, col0, p.M, p.N, lane);
         __syncwarp();
     };
@@ -1033,6 +1042,10 @@ static int launch(const void *A, long long lda, int a_mn, const void *B, long lo
   }
   p.c_tma = (p.epi != EPI_RED || p.tma_red) && (p.epi != EPI_PUSH || p.push_tma) && c_aligned;
   p.h_tma = p.epi == EPI_GELU && !((reinterpret_cast<uintptr_t>(H) & 15u) || ((ldh * 2) & 15));
+  // whole rows end on a 16-byte boundary: every box may go through TMA; else only
+  // the boxes that end inside the row (the last column box is stored per element)
+  const bool row_end_aligned = ((p.N * ce) % 16 == 0) && (p.epi != EPI_GELU || (p.N * 2) % 16 == 0);
+  p.tma_cols = row_end_aligned ? p.N : (p.N / 32) * 32;
   memset(&mc, 0, sizeof mc);
   memset(&mh, 0, sizeof mh);
   if (p.c_tma && (st = p.c_f32 ? make_map(&mc, C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.N, p.M, ldc,

@@ -124,3 +124,27 @@ def test_gemms_write_only_their_views(lib, n):
     for buf in (Hraw, Yraw, Draw):
         pad = buf[GUARD:GUARD + T * npad * 2].view(T, npad * 2)[:, n * 2:]
         assert bool(torch.all(pad == PATTERN)), "a GEMM wrote into its output's pitch padding"
+
+
+@pytest.mark.parametrize("h", [40, 72, 512])
+def test_wgrad_into_bf16_arena_keeps_neighbouring_half_units(lib, h):
+    """Unit-major bf16 arena [n, 2, h]: the dB GEMM writes rows of h elements
+    with a 2h pitch, next to the same unit's (and the next unit's) A half,
+    which must stay untouched.  (Here a row always ends on a 16-byte boundary,
+    because the G operand's own pitch, h elements, must be 16-byte aligned for
+    TMA; the H/Y/D case above is the one whose rows end mid-granule.)"""
+    from paper_2504_06095_b200.linear import mm
+    n, T = 104, 256  # Y's pitch (n elements) must be 16-byte aligned for TMA
+    X = torch.randn((T, h), device="cuda").to(torch.bfloat16)
+    Y = torch.randn((T, n), device="cuda").to(torch.bfloat16)
+    G = torch.randn((T, h), device="cuda").to(torch.bfloat16)
+    gb, graw = guarded(n * 2 * h, torch.bfloat16)
+    grads = gb.view(n, 2, h)
+    mm(Y.T, G.T, grads[:, 1, :])
+    torch.cuda.synchronize()
+    a_half = graw[GUARD:GUARD + n * 2 * h * 2].view(n, 2, h * 2)[:, 0, :]
+    assert bool(torch.all(a_half == PATTERN)), "dB GEMM spilled into the A half"
+    want = (Y.float().T @ G.float())
+    assert torch.allclose(grads[:, 1, :].float(), want, rtol=2e-2, atol=2e-2 * want.abs().max().item())
+    assert guards_intact(graw, n * 2 * h * 2)
+    del X
