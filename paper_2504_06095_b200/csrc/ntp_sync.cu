@@ -192,6 +192,21 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
 __device__ __forceinline__ void st_release_sys(uint64_t *p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// A release pattern for several flag words: ONE system-scope acq_rel fence,
+// then relaxed system-scope stores.  (st.release.sys per word compiles to a
+// MEMBAR.ALL.SYS per word, and __threadfence_system() to a MEMBAR.SC.SYS on
+// top: each costs microseconds on a peer-memory path; SASS-checked.)
+__device__ __forceinline__ void fence_acq_rel_sys() {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(uint64_t *p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void release_words(uint64_t *const *w, int n, uint64_t v) {
+  if (n == 0) return;
+  fence_acq_rel_sys();
+  for (int i = 0; i < n; ++i) st_relaxed_sys(w[i], v);
+}
 __device__ __forceinline__ uint64_t global_timer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -228,9 +243,7 @@ __device__ bool wait_signals(uint64_t *const *wait, int n, uint64_t epoch, uint6
 // the plan kernels
 
 __device__ __forceinline__ void post_signals(uint64_t *const *post, int n, uint64_t epoch) {
-  if (n == 0) return;
-  __threadfence_system();
-  for (int i = 0; i < n; ++i) st_release_sys(post[i], epoch);
+  release_words(post, n, epoch);
 }
 
 // The plan's 256-byte counter block: u32 word 0 counts finished CTAs of the
@@ -245,12 +258,12 @@ __device__ __forceinline__ unsigned int *failed_ctas(const SignalArgs &sig) { re
 // then time out too instead of consuming a partly reduced result, and every
 // process's status reports the failure.
 __device__ __forceinline__ void last_cta_finish(const SignalArgs &sig) {
-  __threadfence_system();
+  fence_acq_rel_sys();  // acquire: every CTA's fenced stores happen-before what follows
   const uint64_t e = sig_epoch(sig);
   const unsigned int failed = atomicExch(failed_ctas(sig), 0u);
   *sig.counter = 0u;
   if (!failed) {
-    for (int i = 0; i < sig.n_post; ++i) st_release_sys(sig.post[i], e);
+    release_words(sig.post, sig.n_post, e);
     if (sig.n_fin) wait_signals(sig.fin, sig.n_fin, e, sig.spin_ns, sig.status);
   }
   sig_advance(sig, e);  // every CTA has read the word: it is safe to move on
@@ -294,7 +307,7 @@ __device__ __forceinline__ bool cta_prologue(const SignalArgs &sig) {
 template <bool kSignaled>
 __device__ __forceinline__ void cta_epilogue(const SignalArgs &sig) {
   if constexpr (kSignaled) {
-    __threadfence_system();  // this thread's peer/local stores, system scope
+    fence_acq_rel_sys();  // release this thread's peer/local stores, system scope
     __syncthreads();
     if (threadIdx.x == 0) {
       const unsigned int done = atomicAdd(sig.counter, 1u);
@@ -500,7 +513,7 @@ plan_kernel_bulk(const Chunk *__restrict__ chunks, int n_chunks, BufTable bufs,
     if constexpr (kSignaled) {
       // async-proxy (bulk) global writes -> generic release at system scope
       asm volatile("fence.proxy.async.global;" ::: "memory");
-      __threadfence_system();
+      fence_acq_rel_sys();
       const unsigned int done = atomicAdd(sig.counter, 1u);
       if (done == gridDim.x - 1) last_cta_finish(sig);
     }
@@ -614,8 +627,7 @@ uniform_kernel(BufTable reps, int R, int64_t n, int op, RepWeights w, int64_t n_
 
 __global__ void signal_post_kernel(SignalArgs sig) {
   const uint64_t e = sig_epoch(sig);
-  __threadfence_system();
-  for (int i = 0; i < sig.n_post; ++i) st_release_sys(sig.post[i], e);
+  release_words(sig.post, sig.n_post, e);
   sig_advance(sig, e);
 }
 
