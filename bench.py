@@ -265,6 +265,8 @@ def run_single(args):
         out["check"] = check_single(args, lay, plan, arenas, dtype)
     if not args.no_e2e:
         out["e2e"] = run_e2e_single(args, lay, plan, dtype, eb)
+        if shape.layers == 1 and not shape.heads:
+            out["e2e_reference_objects"] = run_e2e_reference_objects(args)
     if not args.no_cpu:
         # one whole step of the workload: all layers synced in turn through one
         # layer's host buffers (memory stays at one layer), best of a few (~10 s)
@@ -407,6 +409,44 @@ def run_e2e_single(args, lay, plan, dtype, eb):
             "host_link_duplex_gbs_per_direction": round(duplex_gbs, 1),
             "host_link_bound_ms": round(nbytes / (duplex_gbs * 1e9) * 1e3, 2),
             "host_link_frac": round(nbytes / (duplex_gbs * 1e9) * 1e3 / ms, 3)}
+
+
+def run_e2e_reference_objects(args, reps=20):
+    """C1 through the reference's own call: tpnumerics.nonuniform_grad_sync on
+    replica objects shaped like ntpsim's MlpReplica (numpy fp64 grad_a [h, n_r]
+    / grad_b [n_r, h] lists, mutated in place; tpnumerics.py:131-155,
+    289-356).  The product's host path stages them into pinned unit-major
+    buffers, runs the fp64 kernel and writes the results back (plan and
+    staging cached after the first call); wall time per call."""
+    import torch
+    from types import SimpleNamespace
+    from paper_2504_06095_b200 import tpnumerics as T
+    from paper_2504_06095_b200.shardmap import build_shard_map
+    hidden, ffn = WORKLOADS[args.workload][:2]
+    smap = build_shard_map(ffn, 4, 3)
+    rng = np.random.default_rng(0)
+    layer = T.MlpLayer(np.zeros((hidden, ffn)), np.zeros((ffn, hidden)))
+
+    def replica(cols):
+        return SimpleNamespace(layer=layer, n=len(cols), cols=cols,
+                               grad_a=[rng.standard_normal((hidden, len(c))) for c in cols],
+                               grad_b=[rng.standard_normal((len(c), hidden)) for c in cols])
+    h, r = replica(T.assignment_from_comp(smap)), replica(T.assignment_from_sync(smap))
+    T.nonuniform_grad_sync(h, r, smap, weights=(W_H, W_R))  # builds and caches plan + staging
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        T.nonuniform_grad_sync(h, r, smap, weights=(W_H, W_R))
+        ts.append(time.perf_counter() - t0)
+    t = float(np.median(ts))
+    elems = ffn * 2 * hidden
+    return {"value": round(elems * 8 / t / 1e9, 3), "unit": "GB/s", "dtype": "f64",
+            "ms_per_call_median": round(t * 1e3, 3), "calls": reps,
+            "h2d_bytes_per_step": 2 * elems * 8, "d2h_bytes_per_step": 2 * elems * 8,
+            "note": "wall time of tpnumerics.nonuniform_grad_sync on ntpsim-shaped numpy "
+                    "replicas (fp64, in place): host restaging + H2D + kernel + D2H; the "
+                    "reference's own Python call takes 405 ms on this shape (BASELINE.md)"}
 
 
 def _ncu_traffic(workload):

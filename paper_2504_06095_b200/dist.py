@@ -235,7 +235,7 @@ class NtpSyncGroup:
 
     def __init__(self, lay: PairLayout, placement: Placement, dtype: torch.dtype, device: int,
                  ops: DeviceOps | None = None, group=None, policy: str = "split",
-                 pieces=None, aligned: str = "peer"):
+                 pieces=None, aligned: str = "peer", prescaled: bool = False):
         """pieces: optional list of segment-index lists.  Each piece gets its
         own plan, so a caller can sync piece i as soon as its gradients (or its
         host-to-device copies) are in place: ``step(..., piece=i)``.  Every
@@ -246,7 +246,12 @@ class NtpSyncGroup:
         healthy/reduced arena pair with an NCCL all-reduce (aligned_all_reduce,
         the fall-through of uniform_grad_sync, tpnumerics.py:263-286) instead
         of the peer-memory kernel; "peer" (default, measured faster on B200:
-        DESIGN.md 5) keeps the kernel.  Ignored when n1 != n2."""
+        DESIGN.md 5) keeps the kernel.  Ignored when n1 != n2.
+
+        prescaled (aligned="nccl" only): the gradients already carry their
+        replica's batch weight (folded into the wgrad GEMM's alpha, e.g.
+        MlpShard.backward(alpha=w)), so step() runs a plain NCCL SUM with no
+        weighting pass; step()'s weights are then ignored."""
         if aligned not in ("peer", "nccl"):
             raise ValueError(f"aligned must be 'peer' or 'nccl', got {aligned!r}")
         self.pieces = [sorted(int(i) for i in p) for p in pieces] if pieces else []
@@ -298,6 +303,7 @@ class NtpSyncGroup:
         self._sig_arrays = None
         self._bufs_array = None
         self.aligned = aligned if lay.n1 == lay.n2 else "peer"
+        self.prescaled = bool(prescaled) and self.aligned == "nccl"
         self._aligned_pairs = self._aligned_groups(group) if self.aligned == "nccl" else None
 
     def _build_plans(self, policy) -> None:
@@ -372,7 +378,8 @@ class NtpSyncGroup:
                     if rng is not None:
                         a, b = a[slice(*rng[hs])], b[slice(*rng[rs])]
                     L = _lib.load()
-                    w = (ctypes.c_double * 2)(float(w_h), float(w_r))
+                    w = (ctypes.c_double * 2)(*((1.0, 1.0) if self.prescaled
+                                                else (float(w_h), float(w_r))))
                     _lib.check(L.ntp_uniform_sync(_lib.ptr_array([a.data_ptr(), b.data_ptr()]), 2,
                                                   a.numel(), dtype_code(a.dtype), OPS["weighted"],
                                                   w, ctypes.c_void_p(stream.cuda_stream)),
@@ -382,7 +389,8 @@ class NtpSyncGroup:
                 t = self.arena(slot)
                 if rng is not None:
                     t = t[slice(*rng[slot])]
-                aligned_all_reduce(t, w_h if slot < n1 else w_r, group=grp)
+                aligned_all_reduce(t, None if self.prescaled else (w_h if slot < n1 else w_r),
+                                   group=grp)
 
     def set_policy(self, policy) -> "NtpSyncGroup":
         """Rebuild the plans for another executor policy (same arenas, same

@@ -175,9 +175,11 @@ class MlpShard:
             mm(Y, self.W[:, 1, :].T, Z)
 
     def backward(self, X: torch.Tensor, G: torch.Tensor, grads: torch.Tensor,
-                 pdl: str | None = None) -> None:
+                 pdl: str | None = None, alpha: float = 1.0) -> None:
         """Weight gradients written unit-major into grads [n, 2, h] (bf16 or fp32):
-        grads[:, 1, :] = Y^T G, grads[:, 0, :] = D^T X with D = (G B_i^T) * GeLU'(H).
+        grads[:, 1, :] = alpha * Y^T G, grads[:, 0, :] = alpha * D^T X with
+        D = (G B_i^T) * GeLU'(H).  alpha folds a replica's batch weight into the
+        wgrad epilogue (aligned regions then sync with a plain SUM, no scale pass).
 
         pdl: chain the three GEMMs with programmatic dependent launch.  The
         first GEMM takes this mode ("after", or "independent" when the caller
@@ -195,8 +197,8 @@ class MlpShard:
             Dfull = self._D
         D = Dfull[:, :self.n]
         mm(G, self.W[:, 1, :], D, epilogue="dgelu", aux=H, pdl=pdl)
-        mm(Y.T, G.T, grads[:, 1, :], pdl=None if pdl is None else "independent")
-        mm(D.T, X.T, grads[:, 0, :], pdl=None if pdl is None else "after")
+        mm(Y.T, G.T, grads[:, 1, :], alpha=alpha, pdl=None if pdl is None else "independent")
+        mm(D.T, X.T, grads[:, 0, :], alpha=alpha, pdl=None if pdl is None else "after")
 
     def backward_synced(self, X: torch.Tensor, G: torch.Tensor, grads: torch.Tensor, alpha: float,
                         red_buf: torch.Tensor, red_row: torch.Tensor, partner_arenas,

@@ -57,8 +57,12 @@ class OverlappedBackward:
             for li in reversed(range(len(self.layers))):
                 group, shards = self.layers[li]
                 with torch.cuda.stream(main):
-                    for (sh, grads), (X, G) in zip(shards, inputs[li]):
-                        sh.backward(X, G, grads)
+                    # prescaled aligned groups: the batch weight rides on the
+                    # wgrad GEMMs' alpha and the sync is a plain SUM
+                    pre = getattr(group, "prescaled", False)
+                    for slot, (sh, grads), (X, G) in zip(group.hosted, shards, inputs[li]):
+                        alpha = (self.w_h if slot < group.lay.n1 else self.w_r) if pre else 1.0
+                        sh.backward(X, G, grads, alpha=alpha)
                 self.side.wait_stream(main)
                 if li == 0 and self.uncap_last:
                     L.ntp_set_option(1, 0)  # launched after the last GEMM: every SM

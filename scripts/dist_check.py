@@ -46,8 +46,9 @@ def main():
     plc = Placement.default(world, n1, n2)
     dtype = DT[dname]
     grp = NtpSyncGroup(lay, plc, dtype, device=local, policy=policy,
-                       aligned="nccl" if launch == "nccl" else "peer").upload()
-    if launch == "nccl":
+                       aligned="nccl" if launch.startswith("nccl") else "peer",
+                       prescaled=launch == "nccl_pre").upload()
+    if launch.startswith("nccl"):
         assert grp.aligned == ("nccl" if n1 == n2 else "peer")
     rng = np.random.default_rng(0)
     init = [rng.standard_normal(e) for e in list(lay.h_elems) + list(lay.r_elems)]
@@ -57,6 +58,12 @@ def main():
     torch.cuda.synchronize()
     dist.barrier()
     w = (4 / 7, 3 / 7)
+    if launch == "nccl_pre":  # the producer folded the batch weight in (one step)
+        assert steps == 1
+        for sl in grp.hosted:
+            a = grp.arena(sl)
+            a.copy_((a.double() * (w[0] if sl < n1 else w[1])).to(dtype))
+        torch.cuda.synchronize()
     if launch == "graph_multi":  # all steps recorded into one CUDA graph
         grp.step_graph(*w, steps=steps)
     for i in range(steps if launch != "graph_multi" else 0):

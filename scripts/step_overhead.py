@@ -62,8 +62,10 @@ class Config:
         tok_h, tok_r = args.tokens, args.tokens * n2 // n1
         self.w_h, self.w_r = tok_h / (tok_h + tok_r), tok_r / (tok_h + tok_r)
         self.describe.update(tokens_healthy=tok_h, tokens_degraded=tok_r)
-        self.groups = [NtpSyncGroup(lay, plc, torch.bfloat16, local, aligned=aligned).upload()
-                       for _ in range(L)]
+        # uniform NCCL: the batch weight rides on the wgrad GEMMs' alpha and the
+        # all-reduce is a plain SUM (prescaled), as a uniform deployment would do
+        self.groups = [NtpSyncGroup(lay, plc, torch.bfloat16, local, aligned=aligned,
+                                    prescaled=aligned == "nccl").upload() for _ in range(L)]
         g = torch.Generator(device="cuda").manual_seed(rank)
         rng = np.random.default_rng(rank)
         X = {s: torch.randn((tok_h if s < n1 else tok_r, h), generator=g, device="cuda")

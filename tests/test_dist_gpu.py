@@ -56,6 +56,12 @@ def test_two_gpus_aligned_nccl_fallthrough(n1, dtype):
     _run(2, n1, n1, dtype, 2, "nccl")
 
 
+def test_two_gpus_aligned_nccl_prescaled():
+    """prescaled=True: the weights were folded into the producer (wgrad alpha);
+    the aligned sync is a plain NCCL SUM (no weighting pass)."""
+    _run(2, 4, 4, "f32", 1, "nccl_pre")
+
+
 @pytest.mark.parametrize("launch,policy", [("graph", "split"), ("graph_fused", "split"),
                                            ("graph_multi", "split"), ("graph", "healthy")])
 def test_two_gpus_cuda_graph_steps(launch, policy):
