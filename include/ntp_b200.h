@@ -286,7 +286,9 @@ int ntp_gemm_bf16_red(const void *A, int64_t lda, int a_mn, const void *B, int64
 
 /* Tile selection: 1 (default) AUTO -- 256 x 256 CTA-pair tiles (tcgen05
  * cta_group::2, cluster of 2) unless 256 x 128 pair tiles halve the waves;
- * 2 force 256 x 128 pair tiles; 3 force 256 x 256; 0 single-CTA 128 x 256. */
+ * 2 force 256 x 128 pair tiles; 3 force 256 x 256; 4 force 256 x 224
+ * (K-major B; else 256 x 256; measured slower on the C4 shapes); 0 single-CTA
+ * 128 x 256. */
 int ntp_gemm_set_pair(int mode);
 
 /* Cap on the persistent GEMM's CTAs (0 = every SM).  With a sync kernel capped

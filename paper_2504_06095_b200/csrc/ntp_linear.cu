@@ -408,6 +408,12 @@ __device__ __forceinline__ void tc_commit2(uint64_t *bar, uint16_t mask) {
 // tile with tcgen05.mma.cta_group::2 -- each CTA stages its 128 rows of A and
 // half of B, the leader issues the MMAs, both drain their own TMEM half.
 // kEpi: the fused epilogue, one instantiation each (see launch()).
+// TMEM allocations are a power of two columns (>= 32): the two BN-column
+// accumulators of a 224-wide tile take 512.
+__host__ __device__ constexpr uint32_t tmem_cols(int bn) {
+  return 2 * bn <= 32 ? 32u : 2 * bn <= 64 ? 64u : 2 * bn <= 128 ? 128u : 2 * bn <= 256 ? 256u : 512u;
+}
+
 template <int BN, int kPair, int kStg, int kEpi>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
@@ -444,12 +450,12 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     if constexpr (kPair == 2) {
       asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                        smem_u32(&sm.tmem_base)),
-                   "r"(2 * BN));
+                   "r"(tmem_cols(BN)));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     } else {
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                        smem_u32(&sm.tmem_base)),
-                   "r"(2 * BN));
+                   "r"(tmem_cols(BN)));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
   }
@@ -876,9 +882,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   if (warp == 1) {
     tc_fence_after();
     if constexpr (kPair == 2)
-      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols(BN)));
     else
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols(BN)));
   }
 }
 
@@ -1242,7 +1248,14 @@ int dispatch(const void *A, long long lda, int a_mn, const void *B, long long ld
   // ones by 1.3-1.6x on every C4 GEMM even where they lose a wave to quantization
   // (the narrow tile doubles the A-operand bytes per MAC), so AUTO only takes
   // the narrow tile when the wide one would need twice the waves.
-  const bool wide = mode == 3 || (mode == 1 && cost(256) <= 2 * cost(128));
+  const bool wide = mode == 3 || mode == 4 || (mode == 1 && cost(256) <= 2 * cost(128));
+  // 256 x 224 pair tiles (K-major B only: an MN-major B box is loaded in 64-row
+  // blocks per CTA) remove the wave quantisation of N = 3584 (14 -> 16 N-tiles:
+  // 448 -> 512 tiles on 74 pairs) but measured 3-9 % slower than 256 x 256 on
+  // the C4 shapes (lower MACs per operand byte; profiles/r02/gemm_bench_c4_bn224.json),
+  // so only the explicit mode 4 takes them
+  const bool n224 = !b_mn && N > 192 && mode == 4;
+  if (n224) return gemm::launch<224, 2, 6>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
   if (N > 128 && mode != 2 && wide)
     return gemm::launch<256, 2, 6>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
   return gemm::launch<128, 2, 8>(A, lda, a_mn, B, ldb, b_mn, C, ldc, H, ld_aux, p, s);
@@ -1325,9 +1338,10 @@ extern "C" int ntp_gemm_set_max_ctas(int n) {
 extern "C" int ntp_gemm_get_max_ctas(void) { return gemm::g_max_ctas.load(); }
 
 // 1 (default): CTA-pair tiles (tcgen05 cta_group::2), width picked per shape;
-// 0: 1-SM tiles; 2 / 3: force 256x128 / 256x256 pair tiles.
+// 0: 1-SM tiles; 2 / 3 / 4: force 256x128 / 256x256 / 256x224 pair tiles
+// (224 only with a K-major B operand; otherwise 256).
 extern "C" int ntp_gemm_set_pair(int mode) {
-  if (mode < 0 || mode > 3) return fail(NTP_EINVAL, "pair mode must be 0..3");
+  if (mode < 0 || mode > 4) return fail(NTP_EINVAL, "pair mode must be 0..4");
   gemm::g_pair.store(mode);
   return NTP_OK;
 }

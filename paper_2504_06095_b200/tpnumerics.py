@@ -384,8 +384,12 @@ def nonuniform_grad_sync(healthy, reduced, smap: ShardMap, op: str = "sum",
 
 class _HostPath:
     """Device resources of the reference-object path for one (layout, hidden):
-    the fp64 plan (built and uploaded once), pinned unit-major staging buffers
-    and device arenas, all reused call after call."""
+    the fp64 plan (built and uploaded once), the unit-major device arenas and
+    per-fragment device staging, all reused call after call.  The reference's
+    fragments are copied to and from the device as they lie (grad_a [h, n_r]
+    and grad_b [n_r, h], C-contiguous): the A-half transposes run on the device
+    and the results land straight in the caller's arrays -- no host-side
+    restaging."""
 
     def __init__(self, healthy, reduced, k: int, device: torch.device):
         h = healthy.layer.hidden
@@ -394,8 +398,8 @@ class _HostPath:
         plan = build_pair_plan(healthy.cols, reduced.cols, k, 2 * h, _lib.NTP_F64)
         self.plan = plan.finalize().upload(device.index)
         sizes = [len(c) for c in list(healthy.cols) + list(reduced.cols)]
-        self.host = [torch.empty((n, 2 * h), dtype=torch.float64).pin_memory() for n in sizes]
         self.dev = [torch.empty((n, 2 * h), dtype=torch.float64, device=device) for n in sizes]
+        self.ga = [torch.empty((h, n), dtype=torch.float64, device=device) for n in sizes]
         self.ptrs = tensor_ptrs(self.dev)
         self.stream = torch.cuda.Stream(device)
         self.bytes = sum(n * 2 * h * 8 for n in sizes)
@@ -403,22 +407,27 @@ class _HostPath:
     def run(self, healthy, reduced, code, w_h, w_r) -> None:
         h = self.h
         frags = [(ga, gb) for rep in (healthy, reduced) for ga, gb in zip(rep.grad_a, rep.grad_b)]
-        stage = [t.numpy() for t in self.host]
-        for st, (ga, gb) in zip(stage, frags):   # reference layout -> unit-major (host)
-            st[:, :h] = np.asarray(ga).T
-            st[:, h:] = gb
+        host = [(torch.from_numpy(np.ascontiguousarray(ga, dtype=np.float64)),
+                 torch.from_numpy(np.ascontiguousarray(gb, dtype=np.float64))) for ga, gb in frags]
         s = self.stream
         s.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(s):
-            for d, t in zip(self.dev, self.host):
-                d.copy_(t, non_blocking=True)
+            for d, ga_d, (ga, gb) in zip(self.dev, self.ga, host):
+                ga_d.copy_(ga)                    # [h, n_r] as the caller holds it
+                d[:, h:].copy_(gb)                # B rows: already unit-major
+                d[:, :h].copy_(ga_d.T)            # A columns -> unit-major, on the device
             self.plan.grad_sync(self.ptrs, code, w_h, w_r, s)
-            for d, t in zip(self.dev, self.host):
-                t.copy_(d, non_blocking=True)
-        s.synchronize()
-        for st, (ga, gb) in zip(stage, frags):   # back into the caller's arrays, in place
-            ga[...] = st[:, :h].T
-            gb[...] = st[:, h:]
+            for d, ga_d in zip(self.dev, self.ga):
+                ga_d.copy_(d[:, :h].T)
+        for (ga, gb), (ga_t, gb_t), d, ga_d in zip(frags, host, self.dev, self.ga):
+            with torch.cuda.stream(s):
+                ga_t.copy_(ga_d)                  # device -> the caller's memory
+                gb_t.copy_(d[:, h:])
+            s.synchronize()
+            if ga_t.data_ptr() != np.asarray(ga).__array_interface__["data"][0]:
+                ga[...] = ga_t.numpy()            # the caller's array was not contiguous fp64
+            if gb_t.data_ptr() != np.asarray(gb).__array_interface__["data"][0]:
+                gb[...] = gb_t.numpy()
 
 
 _HOST_PATHS: dict = {}

@@ -61,7 +61,8 @@ def main():
         for name, ours, ref, M, N, K in cases:
             fl = 2.0 * M * N * K
             modes = {}
-            for mode, name_m in ((0, "single_256"), (2, "pair_128"), (3, "pair_256"), (1, "auto")):
+            for mode, name_m in ((0, "single_256"), (2, "pair_128"), (3, "pair_256"), (4, "pair_224"),
+                                 (1, "auto")):
                 _lib.load().ntp_gemm_set_pair(mode)
                 modes[name_m] = timed(ours)
             _lib.load().ntp_gemm_set_split_k(0)

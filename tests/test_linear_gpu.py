@@ -14,7 +14,7 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module", params=[3, 2, 0], ids=["pair256", "pair128", "single"])
+@pytest.fixture(scope="module", params=[3, 2, 4, 0], ids=["pair256", "pair128", "pair224", "single"])
 def Lin(request):
     """Both tile paths: CTA pairs (tcgen05 cta_group::2) and single CTAs."""
     if not torch.cuda.is_available():
