@@ -19,6 +19,7 @@ It imports the reference package ``ntpsim`` read-only from
 * c1_digest.json   -- sha256 of the reference's C1 gradients before and after
                       nonuniform_grad_sync (h1024, k4096, TP4/TP3).
 * golden_mlp.json   -- the reference's own frozen fixture (configs/golden_mlp.json).
+* comm_comp_ratio.json -- perfmodel.comm_comp_ratio (perfmodel.py:244-278) values.
 
 Nothing on the GPU box reads /root/reference: tests use only these files.
 """
@@ -193,10 +194,31 @@ def c1_digest():
         json.dump(doc, f, indent=1)
 
 
+def comm_comp():
+    """perfmodel.comm_comp_ratio (perfmodel.py:244-278): the reference's byte
+    accounting of the busiest reshard rank over backward FLOPs."""
+    from ntpsim.perfmodel import ModelShape, comm_comp_ratio
+    cases = []
+    for hidden, layers, heads, ffn in ((2048, 24, 16, 8192), (4096, 32, 32, 14336),
+                                       (12288, 96, 96, None), (1024, 4, 8, 4096)):
+        shape = ModelShape(hidden=hidden, layers=layers, heads=heads, ffn=ffn)
+        for n1, n2, pp, lb, seq, b in ((4, 3, 1, 4, 2048, 2), (8, 6, 4, 2, 4096, 2),
+                                       (4, 4, 1, 4, 2048, 2), (32, 30, 8, 1, 8192, 2),
+                                       (8, 7, 2, 8, 1024, 4)):
+            if n1 > heads:
+                continue
+            cases.append({"shape": [hidden, layers, heads, ffn], "n1": n1, "n2": n2, "pp": pp,
+                          "local_batch": lb, "seq_len": seq, "bytes_per_element": b,
+                          "ratio": comm_comp_ratio(shape, n1, n2, pp, lb, seq, b)})
+    with open(os.path.join(OUT, "comm_comp_ratio.json"), "w") as f:
+        json.dump(cases, f, indent=1)
+
+
 if __name__ == "__main__":
     shutil.copy(os.path.join(REF, "ntpsim", "configs", "golden_mlp.json"),
                 os.path.join(OUT, "golden_mlp.json"))
     shardmaps()
     sync_cases()
     c1_digest()
+    comm_comp()
     print("fixtures written to", OUT)
