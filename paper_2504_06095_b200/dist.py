@@ -545,6 +545,8 @@ class NtpSyncGroup:
         key = (piece, float(w_h), float(w_r), int(steps), bool(self.fused_step), prologue)
         g = self._graphs.get(key)
         if g is None:
+            if len(self._graphs) >= 16:  # e.g. a caller passing a new prologue each time
+                self._graphs.clear()
             g = torch.cuda.CUDAGraph()
             cap = torch.cuda.Stream(self.device)
             cap.wait_stream(s)
@@ -608,6 +610,9 @@ class NtpSyncGroup:
             self.ops.free(p)
         self.ops.free(self.sig)
         self.local = {}
+        self._graphs = {}
+        # the aligned pairs' NCCL groups stay with the default group, which
+        # destroy_process_group() tears down with every subgroup
 
 
 def aligned_all_reduce(tensor: torch.Tensor, weight: float | None = None, group=None) -> None:

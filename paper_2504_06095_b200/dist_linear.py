@@ -131,7 +131,9 @@ class TpMlpForward:
 
     def forward(self, X: torch.Tensor, stream=None) -> torch.Tensor:
         """Z = sum_r GeLU(X A_r) B_r (fp32 [T, h], identical on every rank) for
-        bf16 X [T, h] (the same X on every rank).  Stream-ordered on `stream`."""
+        bf16 X [T, h] (the same X on every rank).  Stream-ordered on `stream`.
+        The returned tensor is this rank's (IPC-shared) output buffer: the next
+        forward overwrites it, so consume or copy it first."""
         if tuple(X.shape) != (self.T, self.h) or X.dtype != torch.bfloat16:
             raise ValueError(f"X must be bf16 [{self.T}, {self.h}]")
         s = torch.cuda.current_stream(self.device) if stream is None else stream
