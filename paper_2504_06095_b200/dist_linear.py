@@ -51,9 +51,16 @@ class TpMlpForward:
     ``assignment_from_sync(smap)`` for the degraded TP-n2 one)."""
 
     def __init__(self, A: np.ndarray, B: np.ndarray, cols_per_rank, tokens: int, device: int,
-                 group=None, mode: str = "push"):
+                 group=None, mode: str = "push", out_dtype: torch.dtype = torch.float32):
+        """out_dtype: the partial sums' and Z's type -- float32 (default; the
+        reference sums in fp64) or bfloat16 (half the all-reduce bytes, as
+        Megatron-style TP does; the owner still accumulates in fp32)."""
         if mode not in ("push", "nccl"):
             raise ValueError(f"mode must be 'push' or 'nccl', got {mode!r}")
+        if out_dtype not in (torch.float32, torch.bfloat16):
+            raise ValueError("out_dtype must be torch.float32 or torch.bfloat16")
+        self.out_dtype = out_dtype
+        eb = 4 if out_dtype == torch.float32 else 2
         self.group, self.mode, self.device = group, mode, device
         self.rank = dist.get_rank(group)
         self.n = dist.get_world_size(group)
@@ -71,13 +78,13 @@ class TpMlpForward:
         self.blocks = [(min(self.T, j * self.Tb), min(self.T, (j + 1) * self.Tb))
                        for j in range(self.n)]
         self.ops = DeviceOps(device)
-        zb = self.T * self.h * 4
+        zb = self.T * self.h * eb
         self._z = self.ops.alloc(zb)
-        self.Z = _wrap(self._z, self.T * self.h, torch.float32, device).view(self.T, self.h)
+        self.Z = _wrap(self._z, self.T * self.h, out_dtype, device).view(self.T, self.h)
         self.epoch = 0
         if mode == "nccl":
             return
-        self._stg = self.ops.alloc(self.n * self.Tb * self.h * 4)
+        self._stg = self.ops.alloc(self.n * self.Tb * self.h * eb)
         self._sig = self.ops.alloc(_SIG_BYTES)
         mine = {"z": self.ops.handle(self._z), "stg": self.ops.handle(self._stg),
                 "sig": self.ops.handle(self._sig)}
@@ -95,17 +102,17 @@ class TpMlpForward:
         dev = f"cuda:{device}"
         self.red_buf = torch.from_numpy(red_buf).to(dev)
         self.red_row = torch.from_numpy(red_row).to(dev)
-        slot = self.rank * self.Tb * self.h * 4
+        slot = self.rank * self.Tb * self.h * eb
         self.red_bases = [(self.peer_stg[j] + slot) if j != self.rank else (self._stg + slot)
                           for j in range(self.n)]
         # owner reduce: slot r of the own staging, except slot `rank` = own Z rows;
         # the sum goes to the own block's rows of every rank's Z (own first)
         lo, hi = self.blocks[self.rank]
         self._own_rows = (lo, hi)
-        srcs = [self._z + lo * self.h * 4 if r == self.rank
-                else self._stg + r * self.Tb * self.h * 4 for r in range(self.n)]
+        srcs = [self._z + lo * self.h * eb if r == self.rank
+                else self._stg + r * self.Tb * self.h * eb for r in range(self.n)]
         self._srcs = _lib.ptr_array(srcs)
-        dsts = [self._z + lo * self.h * 4] + [self.peer_z[j] + lo * self.h * 4 for j in self.peers]
+        dsts = [self._z + lo * self.h * eb] + [self.peer_z[j] + lo * self.h * eb for j in self.peers]
         self._dsts = _lib.ptr_array(dsts)
         # signal words: region g, writer w -> page + 8*(g*_WORDS + w)
         self._post = {g: _lib.u64_ptr_array([self.peer_sig[j] + 8 * (g * _WORDS + self.rank)
@@ -159,7 +166,7 @@ class TpMlpForward:
             lo, hi = self._own_rows
             if hi > lo:
                 _lib.check(_lib.load().ntp_reduce_into(
-                    self._srcs, self.n, (hi - lo) * self.h, dtype_code(torch.float32),
+                    self._srcs, self.n, (hi - lo) * self.h, dtype_code(self.out_dtype),
                     self._dsts, self.n, ctypes.c_void_p(s.cuda_stream)), "ntp_reduce_into")
             # 4. every block has landed in this rank's Z
             self._signal(_REDUCED, "post", s)

@@ -4,7 +4,7 @@ all-reduce (dist_linear mode "push") against the NCCL baseline (mode "nccl")
 and the two GEMMs alone (no all-reduce: the floor).  Device-timed with CUDA
 events, max over ranks, modes interleaved over rounds.
 
-    torchrun --nproc-per-node N scripts/tp_forward_bench.py [tokens rounds layout]
+    torchrun --nproc-per-node N scripts/tp_forward_bench.py [tokens rounds layout out_dtype]
 """
 
 import json
@@ -44,11 +44,12 @@ def main():
     rng = np.random.default_rng(0)
     A = rng.standard_normal((h, k), dtype=np.float32) / np.sqrt(h)
     B = rng.standard_normal((k, h), dtype=np.float32) / np.sqrt(k)
-    push = TpMlpForward(A, B, cols, T, local, mode="push")
-    nccl = TpMlpForward(A, B, cols, T, local, mode="nccl")
+    odt = {"f32": torch.float32, "bf16": torch.bfloat16}[sys.argv[4] if len(sys.argv) > 4 else "f32"]
+    push = TpMlpForward(A, B, cols, T, local, mode="push", out_dtype=odt)
+    nccl = TpMlpForward(A, B, cols, T, local, mode="nccl", out_dtype=odt)
     X = torch.randn(T, h, device="cuda").to(torch.bfloat16)
     sh = push.shard
-    Zl = torch.empty(T, h, device="cuda")
+    Zl = torch.empty(T, h, device="cuda", dtype=odt)
 
     def gemms():
         sh.activations(X)
@@ -73,16 +74,16 @@ def main():
     assert push.status() == 0
     diff = (push.forward(X) - nccl.forward(X)).abs().max().item()
     flops = 2 * 2 * T * h * sh.n
-    zbytes = T * h * 4
+    zbytes = T * h * (4 if odt == torch.float32 else 2)
     if rank == 0:
-        out = {"what": "TP MLP forward across GPUs, Llama-3-8B MLP shape, bf16 GEMMs, fp32 Z",
+        out = {"what": f"TP MLP forward across GPUs, Llama-3-8B MLP shape, bf16 GEMMs, {odt} Z",
                "n_gpus": n, "tokens": T, "hidden": h, "ffn": k, "layout": layout,
                "cols_per_rank": [len(c) for c in cols], "rounds": rounds, "iters": iters,
                "median_ms": {m: round(float(np.median(v)), 4) for m, v in res.items()},
                "min_ms": {m: round(float(np.min(v)), 4) for m, v in res.items()},
                "all_ms": {m: [round(x, 4) for x in v] for m, v in res.items()},
                "gemm_tflops_rank0": round(flops / (np.median(res["gemms_only"]) * 1e-3) / 1e12, 1),
-               "allreduce_bytes_fp32": zbytes,
+               "allreduce_bytes": zbytes,
                "push_vs_nccl_max_abs_diff": diff}
         out["comm_exposed_ms"] = {m: round(out["median_ms"][m] - out["median_ms"]["gemms_only"], 4)
                                   for m in ("push", "nccl")}

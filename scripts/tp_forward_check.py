@@ -6,7 +6,7 @@ pushes partial-sum boxes to the row-block owners over NVLink; or nccl), and
 checks Z against the fp64 oracle of mlp_forward_dense (tpnumerics.py:170-185)
 on the same bf16-rounded inputs (<= 2e-2), bit-identical across ranks.
 
-    torchrun --nproc-per-node N scripts/tp_forward_check.py [mode layout tokens]
+    torchrun --nproc-per-node N scripts/tp_forward_check.py [mode layout tokens out_dtype]
 layout: "comp" (healthy TP-N columns of build_shard_map(k, N, N-1)) or
 "sync" (the degraded replica's contiguous columns of build_shard_map(k, N+1, N))
 """
@@ -30,6 +30,7 @@ def main():
     mode = sys.argv[1] if len(sys.argv) > 1 else "push"
     layout = sys.argv[2] if len(sys.argv) > 2 else "sync"
     T = int(sys.argv[3]) if len(sys.argv) > 3 else 512
+    out_dtype = {"f32": torch.float32, "bf16": torch.bfloat16}[sys.argv[4] if len(sys.argv) > 4 else "f32"]
     os.environ["NCCL_DEBUG"] = "WARN"
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -43,7 +44,7 @@ def main():
     rng = np.random.default_rng(9)  # identical on every rank
     r64 = lambda x: torch.from_numpy(x).to(torch.bfloat16).double().numpy()  # noqa: E731
     A, B = r64(rng.standard_normal((h, k)) / np.sqrt(h)), r64(rng.standard_normal((k, h)) / np.sqrt(k))
-    tp = TpMlpForward(A, B, cols, T, local, mode=mode)
+    tp = TpMlpForward(A, B, cols, T, local, mode=mode, out_dtype=out_dtype)
     ok = True
     for it in range(3):
         X = r64(rng.standard_normal((T, h)))
@@ -51,13 +52,13 @@ def main():
         torch.cuda.synchronize()
         assert tp.status() == 0, "signal timeout"
         want = O.mlp_forward_dense(X, A, B)
-        err = O.rel_err(Z.double().cpu().numpy(), want)
+        err = O.rel_err(Z.double().cpu().numpy(), want)  # <= 2e-2 (bf16 operands)
         allz = [torch.empty_like(Z) for _ in range(n)]
         dist.all_gather(allz, Z)
         same = all(torch.equal(allz[0], z) for z in allz)
         ok &= err <= 2e-2 and same
         if rank == 0:
-            print(f"tp_forward n={n} {mode} {layout} T={T} iter={it} rel_err={err:.3e} "
+            print(f"tp_forward n={n} {mode} {layout} T={T} {out_dtype} iter={it} rel_err={err:.3e} "
                   f"identical={same}", flush=True)
     tp.close()
     if rank == 0:

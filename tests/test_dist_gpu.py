@@ -131,6 +131,13 @@ def test_row_parallel_forward_multi_gpu(n, mode, layout, tokens):
     _run_script(n, "tp_forward_check.py", mode, layout, tokens)
 
 
+@pytest.mark.parametrize("n,mode", [(2, "push"), (4, "push"), (2, "nccl")])
+def test_row_parallel_forward_bf16_partials(n, mode):
+    """out_dtype=bf16: bf16 partial sums and Z (half the all-reduce bytes), the
+    owner still accumulates in fp32; <= 2e-2 of the oracle, identical on every rank."""
+    _run_script(n, "tp_forward_check.py", mode, "sync", 512, "bf16")
+
+
 @pytest.mark.parametrize("n,n1,dead", [(1, 4, 3), (2, 4, 1), (4, 2, 0)])
 def test_failure_reconfig_multi_gpu(n, n1, dead):
     """dist_reconfig: H -> comp layout, D's survivors -> TP-(n1-1), the dead
