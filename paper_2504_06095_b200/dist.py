@@ -542,6 +542,10 @@ class NtpSyncGroup:
                 self.step(w_h, w_r, stream, piece=piece)
             return
         s = torch.cuda.current_stream(self.device) if stream is None else stream
+        plan = self.plan if piece is None else self.piece_plans[piece]
+        if plan is None and not self.partners and prologue is None:
+            self.epoch += steps  # nothing to run here (e.g. the idle GPU at N=8)
+            return
         key = (piece, float(w_h), float(w_r), int(steps), bool(self.fused_step), prologue)
         g = self._graphs.get(key)
         if g is None:
