@@ -58,7 +58,9 @@ int ntp_abi_version(void);
 /* Process-wide tuning knobs (no reference counterpart). */
 enum ntp_option {
   NTP_OPT_SYNC_KERNEL = 0,   /* value: enum ntp_sync_kernel */
-  NTP_OPT_SYNC_MAX_CTAS = 1  /* value: cap on sync-kernel CTAs, 0 = all SMs */
+  NTP_OPT_SYNC_MAX_CTAS = 1,  /* value: cap on sync-kernel CTAs, 0 = all SMs */
+  NTP_OPT_PLAN_MIN_CHUNKS = 2 /* value: plans finalized afterwards get at least this many
+                                 chunks (smaller chunks, >= 64 grains); 0 = 16 KiB chunks */
 };
 enum ntp_sync_kernel {
   NTP_KERNEL_AUTO = 0,  /* default: LDG below 4 chunks per SM, BULK above */

@@ -16,6 +16,8 @@ static thread_local std::string g_last_error;
 
 void set_error(const std::string &msg) { g_last_error = msg; }
 
+std::atomic<int64_t> g_min_chunks{0};
+
 int fail(int status, const std::string &msg) {
   set_error(msg);
   return status;
@@ -250,7 +252,15 @@ int ntp_plan_finalize(ntp_plan *p) {
   for (const Run &r : p->runs)
     if (r.a_off % vec || r.b_off % vec || r.len % vec) vectorized = false;
   const int64_t grain = vectorized ? vec : 1;
-  const int64_t chunk = vectorized ? kChunkVecs : kChunkElems;
+  int64_t chunk = vectorized ? kChunkVecs : kChunkElems;
+  const int64_t min_chunks = g_min_chunks.load();
+  if (min_chunks > 0) {
+    int64_t grains = 0;
+    for (const Run &r : p->runs) grains += r.len / grain;
+    const int64_t floor_chunk = vectorized ? 64 : 256;
+    if (grains / chunk < min_chunks)
+      chunk = std::max<int64_t>(floor_chunk, std::min<int64_t>(chunk, grains / min_chunks));
+  }
   p->chunks.clear();
   for (const Run &r : p->runs) {
     const int64_t g = r.len / grain;

@@ -48,6 +48,7 @@ struct BufTable {
 // Cap on sync-kernel CTAs (0 = one wave over all SMs).  Lets a sync that is
 // overlapped with the backward GEMMs leave most SMs to the tensor cores.
 static std::atomic<int> g_max_ctas{0};
+static uint64_t *g_trace = nullptr;  // debug: ntp_debug_sync_trace
 
 struct SignalArgs {
   uint64_t *wait[16];
@@ -69,6 +70,10 @@ struct SignalArgs {
   // the step's final kernel (advance = 1) stores that epoch back
   uint64_t *epoch_word = nullptr;
   int advance = 0;
+  // debug only (ntp_debug_sync_trace, not in the header): globaltimer stamps
+  // [0] CTA 0 start, [1] ready posted, [2] ready seen by CTA 0, [3] last CTA
+  // entered its finish, [4] done posted, [5] partners' done seen
+  uint64_t *trace = nullptr;
 };
 
 enum { OP_COPY = 3 };
@@ -258,13 +263,16 @@ __device__ __forceinline__ unsigned int *failed_ctas(const SignalArgs &sig) { re
 // then time out too instead of consuming a partly reduced result, and every
 // process's status reports the failure.
 __device__ __forceinline__ void last_cta_finish(const SignalArgs &sig) {
+  if (sig.trace) sig.trace[3] = global_timer_ns();
   fence_acq_rel_sys();  // acquire: every CTA's fenced stores happen-before what follows
   const uint64_t e = sig_epoch(sig);
   const unsigned int failed = atomicExch(failed_ctas(sig), 0u);
   *sig.counter = 0u;
   if (!failed) {
     release_words(sig.post, sig.n_post, e);
+    if (sig.trace) sig.trace[4] = global_timer_ns();
     if (sig.n_fin) wait_signals(sig.fin, sig.n_fin, e, sig.spin_ns, sig.status);
+    if (sig.trace) sig.trace[5] = global_timer_ns();
   }
   sig_advance(sig, e);  // every CTA has read the word: it is safe to move on
 }
@@ -291,11 +299,15 @@ __device__ __forceinline__ bool cta_prologue(const SignalArgs &sig) {
       // the first CTA to start posts this process's ready words, so no CTA
       // waits on a post that an unscheduled CTA would make (word 1 of the
       // plan's counter block records the last epoch posted)
+      const bool tr = sig.trace && blockIdx.x == 0;
+      if (tr) sig.trace[0] = global_timer_ns();
       const uint64_t e = sig_epoch(sig);
       if (sig.n_pre && atomicMax(reinterpret_cast<unsigned long long *>(sig.counter) + 1,
                                  (unsigned long long)e) < e)
         post_signals(sig.pre, sig.n_pre, e);
+      if (tr) sig.trace[1] = global_timer_ns();
       ok = wait_signals(sig.wait, sig.n_wait, e, sig.spin_ns, sig.status) ? 1 : 0;
+      if (tr) sig.trace[2] = global_timer_ns();
     }
     __syncthreads();
     return ok != 0;
@@ -791,6 +803,11 @@ using namespace ntp;
 extern "C" {
 
 int ntp_set_option(int option, int64_t value) {
+  if (option == NTP_OPT_PLAN_MIN_CHUNKS) {
+    if (value < 0 || value > 1 << 24) return fail(NTP_EINVAL, "bad minimum chunk count");
+    g_min_chunks.store(value);
+    return NTP_OK;
+  }
   if (option == NTP_OPT_SYNC_MAX_CTAS) {
     if (value < 0 || value > 1 << 20) return fail(NTP_EINVAL, "bad CTA cap");
     g_max_ctas.store((int)value);
@@ -804,6 +821,7 @@ int ntp_set_option(int option, int64_t value) {
 }
 
 int64_t ntp_get_option(int option) {
+  if (option == NTP_OPT_PLAN_MIN_CHUNKS) return g_min_chunks.load();
   if (option == NTP_OPT_SYNC_MAX_CTAS) return g_max_ctas.load();
   if (option != NTP_OPT_SYNC_KERNEL) return fail(NTP_EINVAL, "unknown option");
   return g_sync_kernel.load();
@@ -1010,6 +1028,7 @@ static int grad_sync_signaled(const ntp_plan *p, void *const *bufs, int n_bufs, 
   SignalArgs sig;
   if ((st = fill_signals(sig, wait, n_wait, post, n_post, epoch, spin_ns, status))) return st;
   sig.counter = p->d_counter;
+  sig.trace = g_trace;
   sig.epoch_word = epoch_word;  // never advanced here: the step's done-wait advances
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (p->chunks.empty()) {
@@ -1070,6 +1089,7 @@ static int grad_sync_step(const ntp_plan *p, void *const *bufs, int n_bufs, int 
   if (op < NTP_OP_SUM || op > NTP_OP_WEIGHTED) return fail(NTP_EINVAL, "unknown reduction op");
   if ((st = set_device(p->device))) return st;
   sig.counter = p->d_counter;
+  sig.trace = g_trace;
   if ((st = launch_plan<true>(p, op, bt, w_a, w_b, sig, s))) return st;
   NTP_CUDA(cudaGetLastError());
   return NTP_OK;
@@ -1119,6 +1139,13 @@ static int signal_wait(uint64_t *const *wait, int n_wait, uint64_t epoch, uint64
   if ((st = set_device_of(static_cast<cudaStream_t>(stream)))) return st;
   signal_wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(sig);
   NTP_CUDA(cudaGetLastError());
+  return NTP_OK;
+}
+
+// Debug hook, not in the header: device buffer of >= 6 u64 that signalled
+// sync launches stamp with globaltimer (nullptr: off).
+int ntp_debug_sync_trace(void *buf) {
+  g_trace = static_cast<uint64_t *>(buf);
   return NTP_OK;
 }
 

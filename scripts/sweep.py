@@ -177,7 +177,9 @@ def main():
     ap.add_argument("--reconfig-layers", type=int, default=32)
     ap.add_argument("--sync-only", action="store_true")
     args = ap.parse_args()
-    _lib.load()
+    L = _lib.load()
+    if os.environ.get("NTP_MIN_CHUNKS"):  # experiments: NTP_OPT_PLAN_MIN_CHUNKS
+        _lib.check(L.ntp_set_option(2, int(os.environ["NTP_MIN_CHUNKS"])))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:
