@@ -39,9 +39,10 @@ static_assert(sizeof(Chunk) == 16, "chunk record must be 16 bytes");
 // Grains per chunk: 1024 x 16 B = 16 KiB per side for the vector path.
 constexpr uint32_t kChunkVecs = 1024;
 constexpr uint32_t kChunkElems = 4096;  // scalar path
-// NTP_OPT_PLAN_MIN_CHUNKS: plans finalized while this is > 0 shrink their
-// chunks (down to 64 grains) so the plan has at least this many -- small plans
-// then spread over every SM several times, which shortens the tail.
+// NTP_OPT_PLAN_MIN_CHUNKS (default 1184 = 8 per SM): plans finalized while
+// this is > 0 shrink their chunks (down to 64 grains) so the plan has at least
+// this many -- small plans then spread over every SM several times, which
+// shortens the tail.
 extern std::atomic<int64_t> g_min_chunks;
 
 constexpr int kMaxBufs = 64;

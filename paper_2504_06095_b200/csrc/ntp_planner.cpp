@@ -16,7 +16,7 @@ static thread_local std::string g_last_error;
 
 void set_error(const std::string &msg) { g_last_error = msg; }
 
-std::atomic<int64_t> g_min_chunks{0};
+std::atomic<int64_t> g_min_chunks{1184};  // 8 per SM of a B200 (measured: scripts/sweep.py)
 
 int fail(int status, const std::string &msg) {
   set_error(msg);
@@ -255,11 +255,12 @@ int ntp_plan_finalize(ntp_plan *p) {
   int64_t chunk = vectorized ? kChunkVecs : kChunkElems;
   const int64_t min_chunks = g_min_chunks.load();
   if (min_chunks > 0) {
-    int64_t grains = 0;
-    for (const Run &r : p->runs) grains += r.len / grain;
-    const int64_t floor_chunk = vectorized ? 64 : 256;
-    if (grains / chunk < min_chunks)
-      chunk = std::max<int64_t>(floor_chunk, std::min<int64_t>(chunk, grains / min_chunks));
+    // the target is set in elements, a multiple of 8, so plans over the same
+    // units split identically in every dtype (grains are 2, 4 or 8 elements)
+    int64_t elems = 0;
+    for (const Run &r : p->runs) elems += r.len;
+    const int64_t target = std::max<int64_t>(512, elems / min_chunks / 8 * 8);
+    if (target / grain < chunk) chunk = target / grain;
   }
   p->chunks.clear();
   for (const Run &r : p->runs) {

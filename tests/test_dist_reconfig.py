@@ -86,6 +86,19 @@ def _expected(lay, arenas):
     return want
 
 
+def _merged(tab):
+    """Chunk records (a_buf, a_off, b_buf, b_off, len) merged into maximal runs
+    that are contiguous on both sides."""
+    runs = []
+    for ab, ao, bb, bo, ln in sorted(map(tuple, np.asarray(tab).tolist())):
+        if runs and runs[-1][0] == ab and runs[-1][2] == bb and \
+                runs[-1][1] + runs[-1][4] == ao and runs[-1][3] + runs[-1][4] == bo:
+            runs[-1][4] += ln
+        else:
+            runs.append([ab, ao, bb, bo, ln])
+    return runs
+
+
 @pytest.mark.parametrize("world,n1,dead", [(2, 4, 3), (2, 4, 0), (4, 2, 1), (4, 4, 1)])
 def test_gloo_failure_reconfig_tables(world, n1, dead):
     n2 = n1 - 1
@@ -105,7 +118,9 @@ def test_gloo_failure_reconfig_tables(world, n1, dead):
             continue
         assert set(tabs) == {str(torch.bfloat16), str(torch.float32)}
         t16, t32 = tabs[str(torch.bfloat16)], tabs[str(torch.float32)]
-        np.testing.assert_array_equal(t16, t32)  # one unit table serves every dtype
+        # the same units move in every dtype (chunk boundaries may differ: a
+        # chunk is a byte budget, NTP_OPT_PLAN_MIN_CHUNKS splits small plans)
+        assert _merged(t16) == _merged(t32)
         for ab, ao, bb, bo, ln in t16:
             src, dst = order[ab], order[bb]
             assert proc[dst] == rank                 # pull model: destinations are local
