@@ -24,7 +24,12 @@ def main():
     dtype = bench._torch_dtype(workload)
     eb = bench.ELEM_BYTES[bench.WORKLOADS[workload][4]]
     lay = pair_layout(SHAPES[workload], 4, 3)
-    plan = build_plan(lay, dtype).upload(0)
+    plans = {}
+    for mc in (1184, 4096, 8192, 16384):  # NTP_OPT_PLAN_MIN_CHUNKS
+        _lib.check(L.ntp_set_option(2, mc))
+        plans[mc] = build_plan(lay, dtype).upload(0)
+    _lib.check(L.ntp_set_option(2, 1184))
+    plan = plans[1184]
     arenas = [torch.randn(e, device="cuda").to(dtype) for e in lay.h_elems + lay.r_elems]
     ptrs = tensor_ptrs(arenas)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -50,6 +55,17 @@ def main():
                      "frac_hbm": round(4 * lay.elems * eb / (med * 1e-3) / 1e9 / hbm, 4)}
     _lib.check(L.ntp_set_option(0, 0))
     _lib.check(L.ntp_set_option(1, 0))
+    for mc, pl in plans.items():  # AUTO kernel, smaller chunks
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * steps)]
+        for i in range(steps):
+            flush.fill_(i & 0xFF)
+            ev[2 * i].record()
+            pl.grad_sync(ptrs, OPS["weighted"], 4 / 7, 3 / 7)
+            ev[2 * i + 1].record()
+        torch.cuda.synchronize()
+        ts = sorted(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(steps))
+        out[f"auto_min_chunks_{mc}"] = {"chunks": pl.stats["n_chunks"],
+                                        "us_median": round(ts[len(ts) // 2] * 1e3, 2)}
     print(json.dumps(out, indent=1))
 
 
