@@ -8,7 +8,8 @@ GPU 1) from ONE process over peer-enabled GPUs, unsignalled: GPU 0 runs rank
 0's plan, then GPU 1 runs rank 1's.  Under
 
     ncu --metrics nvltx__bytes.sum,nvlrx__bytes.sum,dram__bytes_read.sum,\\
-        dram__bytes_write.sum,gpu__time_duration.sum python scripts/nvlink_traffic.py
+        dram__bytes_write.sum,gpu__time_duration.sum python scripts/nvlink_traffic.py \\
+        [workload reps world plan.json]
 
 each kernel reports its own GPU's NVLink TX / RX bytes.  With two GPUs one
 link pair carries everything, so during the real (concurrent) step
@@ -35,19 +36,30 @@ from paper_2504_06095_b200.workloads import SHAPES, pair_layout  # noqa: E402
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "gpt-1.3b"
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+    world = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+    plan_out = sys.argv[4] if len(sys.argv) > 4 else None
     _lib.load()
-    for a, b in ((0, 1), (1, 0)):
+    for a in range(world):
         rt.cudaSetDevice(a)
-        rt.cudaDeviceEnablePeerAccess(b, 0)
+        for b in range(world):
+            if a != b:
+                rt.cudaDeviceEnablePeerAccess(b, 0)
     dtype = torch.bfloat16
+    eb = 2
     lay = pair_layout(SHAPES[name], 4, 3)
-    plc = Placement.default(2, 4, 3)
+    plc = Placement.default(world, 4, 3)
     elems = list(lay.h_elems) + list(lay.r_elems)
     arenas = {s: torch.randn(elems[s], device=f"cuda:{plc.proc_of_slot(s)}").to(dtype)
               for s in range(len(elems))}
     plans = []
-    for rank in (0, 1):
+    # algorithmic NVLink bytes of each rank's plan, per peer GPU: a unit executed
+    # on `rank` whose other copy lives on GPU q reads unit*eb from q and writes
+    # unit*eb to q
+    per_peer = {r: {q: 0 for q in range(world)} for r in range(world)}
+    for rank in range(world):
         units, touched = process_plan_units(lay, plc, rank, "split")
+        if not units:
+            continue
         order = sorted(touched)
         remap = np.full(len(elems), -1, dtype=np.int64)
         for i, s in enumerate(order):
@@ -55,7 +67,18 @@ def main():
         p = Plan(dtype_code(dtype))
         for unit, hs, ho, rs, ro in units:
             p.add_units(unit, remap[hs], ho, remap[rs], ro)
+            for slots in (hs, rs):
+                procs = np.array([plc.proc_of_slot(int(x)) for x in range(len(elems))])[slots]
+                for q in np.unique(procs):
+                    if q != rank:
+                        per_peer[rank][int(q)] += int((procs == q).sum()) * unit * eb
         plans.append((rank, p.finalize().upload(rank), [arenas[s].data_ptr() for s in order]))
+    if plan_out:
+        import json
+        with open(plan_out, "w") as f:
+            json.dump({"world": world, "workload": name,
+                       "read_and_write_bytes_per_peer": {str(r): {str(q): v for q, v in d.items()}
+                                                         for r, d in per_peer.items()}}, f)
     for _ in range(reps):
         for rank, p, bufs in plans:
             with torch.cuda.device(rank):
