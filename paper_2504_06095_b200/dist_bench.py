@@ -115,13 +115,13 @@ def run(args):
     # per-process plans (NVML's NVLink throughput counters are not supported on
     # these boxes, and merely querying them slowed the step by 17 %: DESIGN.md 6)
     rec = _ncu_nvlink(args.workload, world)
-    traffic = int(rec["busiest_direction_bytes"]) if rec else None
-    traffic_src = ("ncu nvltx/nvlrx__bytes.sum of this placement's per-process plans "
-                   "(scripts/nvlink_traffic.py, profiles/ncu_nvlink_traffic.json): busiest GPU "
-                   "direction incl. packet overhead; user data only "
-                   f"{int(rec['busiest_direction_user_data_bytes'])} B" if rec else
-                   "not measured at this N (ncu separates per-direction NVLink bytes only "
-                   "for a two-GPU link pair)")
+    traffic = int(rec["busiest_direction_user_data_bytes"]) if rec else None
+    traffic_raw = int(rec["busiest_direction_bytes"]) if rec else None
+    traffic_src = ("ncu nvltx/nvlrx__bytes_data_user.sum of this placement's per-process plans "
+                   "(scripts/nvlink_traffic.py, profiles/ncu_nvlink_traffic.json): payload bytes "
+                   "in the busiest GPU direction; traffic_with_protocol adds NVLink packet "
+                   "overhead (read requests, headers)" if rec else
+                   "not measured for this workload / N")
     kernel_ms = ms
     if grp.status() != 0:
         raise RuntimeError(f"rank {rank}: signal timeout")
@@ -148,6 +148,7 @@ def run(args):
                             "unit": "GB/s", "frac": round(achieved / pk["nvlink_gbs"], 4),
                             "algorithmic_bytes_per_launch": B, "traffic": traffic,
                             "traffic_src": traffic_src,
+                            "traffic_with_protocol": traffic_raw,
                             "traffic_over_algorithmic": (round(traffic / B, 3) if traffic and B
                                                          else None),
                             "kernel_ms": round(kernel_ms, 4)},
