@@ -300,6 +300,9 @@ class NtpSyncGroup:
         # three launches (post ready / signalled sync / wait done), no outliers
         # in the same runs, and no difference at the bench's 2.4 GB.
         self.fused_step = False
+        # CUDA-graph steps only: two launches (ready post, then the sync kernel
+        # whose last CTA posts done and waits for the partners' done)
+        self.two_launch = False
         self._sig_arrays = None
         self._bufs_array = None
         self.aligned = aligned if lay.n1 == lay.n2 else "peer"
@@ -505,10 +508,16 @@ class NtpSyncGroup:
             if plan is not None:
                 plan.grad_sync(self.bufs, OPS["weighted"], w_h, w_r, s)
             return
-        if self.fused_step:
+        if self.fused_step or self.two_launch:
+            # two_launch: the ready post is its own (early) launch and the sync
+            # kernel's last CTA posts done and waits for the partners' done
+            if self.two_launch and not self.fused_step and self.post_ready:
+                _lib.check(L.ntp_signal_post_dev(pr, len(self.post_ready), ew, sp),
+                           "ntp_signal_post_dev")
+            n_pre = len(self.post_ready) if self.fused_step else 0
             _lib.check(L.ntp_grad_sync_step_dev(
                 plan._h if plan is not None else None, bufs, len(self.bufs), OPS["weighted"],
-                float(w_h), float(w_r), pr, len(self.post_ready), wr, len(self.wait_ready),
+                float(w_h), float(w_r), pr, n_pre, wr, len(self.wait_ready),
                 pd, len(self.post_done), wd, len(self.wait_done), ew, spin, st, sp),
                 "ntp_grad_sync_step_dev")
             return
@@ -546,7 +555,8 @@ class NtpSyncGroup:
         if plan is None and not self.partners and prologue is None:
             self.epoch += steps  # nothing to run here (e.g. the idle GPU at N=8)
             return
-        key = (piece, float(w_h), float(w_r), int(steps), bool(self.fused_step), prologue)
+        key = (piece, float(w_h), float(w_r), int(steps), bool(self.fused_step),
+               bool(self.two_launch), prologue)
         g = self._graphs.get(key)
         if g is None:
             if len(self._graphs) >= 16:  # e.g. a caller passing a new prologue each time

@@ -68,6 +68,7 @@ def main():
         grp.step_graph(*w, steps=steps)
     for i in range(steps if launch != "graph_multi" else 0):
         grp.fused_step = launch in ("fused", "graph_fused") or (launch == "alternate" and i % 2 == 0)
+        grp.two_launch = launch == "graph_two"
         if launch.startswith("graph") and i % 2 == 0:
             grp.step_graph(*w)  # graph replays interleaved with eager steps
         else:

@@ -63,7 +63,8 @@ def test_two_gpus_aligned_nccl_prescaled():
 
 
 @pytest.mark.parametrize("launch,policy", [("graph", "split"), ("graph_fused", "split"),
-                                           ("graph_multi", "split"), ("graph", "healthy")])
+                                           ("graph_two", "split"), ("graph_multi", "split"),
+                                           ("graph", "healthy"), ("graph_two", "healthy")])
 def test_two_gpus_cuda_graph_steps(launch, policy):
     """Steps recorded into CUDA graphs with device-resident epochs (the *_dev
     entry points), alone or interleaved with eager steps: same result as the
