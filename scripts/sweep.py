@@ -184,6 +184,8 @@ def main():
     L = _lib.load()
     if os.environ.get("NTP_MIN_CHUNKS"):  # experiments: NTP_OPT_PLAN_MIN_CHUNKS
         _lib.check(L.ntp_set_option(2, int(os.environ["NTP_MIN_CHUNKS"])))
+    if os.environ.get("NTP_SYNC_KERNEL"):  # experiments: 1 LDG, 2 BULK 4x1, 3 BULK 3x2
+        _lib.check(L.ntp_set_option(0, int(os.environ["NTP_SYNC_KERNEL"])))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:
