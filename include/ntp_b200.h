@@ -59,10 +59,12 @@ int ntp_abi_version(void);
 enum ntp_option {
   NTP_OPT_SYNC_KERNEL = 0,   /* value: enum ntp_sync_kernel */
   NTP_OPT_SYNC_MAX_CTAS = 1,  /* value: cap on sync-kernel CTAs, 0 = all SMs */
-  NTP_OPT_PLAN_MIN_CHUNKS = 2 /* value: plans finalized afterwards get at least this many
+  NTP_OPT_PLAN_MIN_CHUNKS = 2, /* value: plans finalized afterwards get at least this many
                                  chunks (smaller chunks, >= 64 grains; default 1184 = 8
                                  per SM: a 16 MB-per-replica N=2 step 47.7 -> 43.1 us);
                                  0 = always 16 KiB chunks */
+  NTP_OPT_SYNC_L2 = 3         /* value: L2 policy of the bulk sync kernel's copies: 0 none
+                                 (default), 1 loads evict_first, 2 loads + stores */
 };
 enum ntp_sync_kernel {
   NTP_KERNEL_AUTO = 0,  /* default: LDG below 4 chunks per SM, BULK above */

@@ -49,6 +49,7 @@ struct BufTable {
 // overlapped with the backward GEMMs leave most SMs to the tensor cores.
 static std::atomic<int> g_max_ctas{0};
 static uint64_t *g_trace = nullptr;  // debug: ntp_debug_sync_trace
+static std::atomic<int> g_l2_hint{0};  // NTP_OPT_SYNC_L2
 
 struct SignalArgs {
   uint64_t *wait[16];
@@ -74,6 +75,9 @@ struct SignalArgs {
   // [0] CTA 0 start, [1] ready posted, [2] ready seen by CTA 0, [3] last CTA
   // entered its finish, [4] done posted, [5] partners' done seen
   uint64_t *trace = nullptr;
+  // L2 policy of the bulk kernel's copies (NTP_OPT_SYNC_L2): 0 none, 1 loads
+  // evict_first, 2 loads and stores evict_first
+  int l2_hint = 0;
 };
 
 enum { OP_COPY = 3 };
@@ -414,6 +418,26 @@ __device__ __forceinline__ void bulk_load(void *smem_dst, const void *gsrc, uint
       "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_load_hint(void *smem_dst, const void *gsrc, uint32_t bytes,
+                                               uint64_t *bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+      "%2, [%3], %4;" ::"r"(smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store_hint(void *gdst, const void *smem_src, uint32_t bytes,
+                                                uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
+                   gdst),
+               "r"(smem_u32(smem_src)), "r"(bytes), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_store(void *gdst, const void *smem_src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
                "r"(smem_u32(smem_src)), "r"(bytes)
@@ -469,6 +493,7 @@ plan_kernel_bulk(const Chunk *__restrict__ chunks, int n_chunks, BufTable bufs,
   if (warp == kBulkConsumers / 32) {
     // ---- producer: one elected lane issues the bulk loads ----
     if ((tid & 31) == 0) {
+      const uint64_t pol = sig.l2_hint ? policy_evict_first() : 0;
       int stage = 0;
       uint32_t phase = 0;
       for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
@@ -479,11 +504,17 @@ plan_kernel_bulk(const Chunk *__restrict__ chunks, int n_chunks, BufTable bufs,
         const uint4 *gb = reinterpret_cast<const uint4 *>(bufs.p[rec.w >> 16]) + rec.y;
         if constexpr (OP == OP_COPY) {
           mbar_expect_tx(&sm.full[stage], bytes);
-          bulk_load(sm.a[stage], ga, bytes, &sm.full[stage]);
+          if (sig.l2_hint) bulk_load_hint(sm.a[stage], ga, bytes, &sm.full[stage], pol);
+          else bulk_load(sm.a[stage], ga, bytes, &sm.full[stage]);
         } else {
           mbar_expect_tx(&sm.full[stage], 2u * bytes);
-          bulk_load(sm.a[stage], ga, bytes, &sm.full[stage]);
-          bulk_load(sm.b[stage], gb, bytes, &sm.full[stage]);
+          if (sig.l2_hint) {
+            bulk_load_hint(sm.a[stage], ga, bytes, &sm.full[stage], pol);
+            bulk_load_hint(sm.b[stage], gb, bytes, &sm.full[stage], pol);
+          } else {
+            bulk_load(sm.a[stage], ga, bytes, &sm.full[stage]);
+            bulk_load(sm.b[stage], gb, bytes, &sm.full[stage]);
+          }
         }
         if (++stage == kStages) { stage = 0; phase ^= 1u; }
       }
@@ -506,7 +537,15 @@ plan_kernel_bulk(const Chunk *__restrict__ chunks, int n_chunks, BufTable bufs,
     if (tid == 0) {
       uint4 *ga = reinterpret_cast<uint4 *>(bufs.p[rec.w & 0xffffu]) + rec.x;
       uint4 *gb = reinterpret_cast<uint4 *>(bufs.p[rec.w >> 16]) + rec.y;
-      if constexpr (OP != OP_COPY) {
+      if (sig.l2_hint == 2) {
+        const uint64_t pol = policy_evict_first();
+        if constexpr (OP != OP_COPY) {
+          if (sig.wmask & 1) bulk_store_hint(ga, sm.a[stage], rec.z * 16u, pol);
+          if (sig.wmask & 2) bulk_store_hint(gb, sm.a[stage], rec.z * 16u, pol);
+        } else {
+          bulk_store_hint(gb, sm.a[stage], rec.z * 16u, pol);
+        }
+      } else if constexpr (OP != OP_COPY) {
         if (sig.wmask & 1) bulk_store(ga, sm.a[stage], rec.z * 16u);
         if (sig.wmask & 2) bulk_store(gb, sm.a[stage], rec.z * 16u);
       } else {
@@ -707,7 +746,9 @@ static int launch_bulk(const ntp_plan *p, const BufTable &bt, typename Acc<T>::t
   const int cap = g_max_ctas.load();
   if (cap > 0 && grid > cap) grid = cap;
   if (n < grid) grid = n > 0 ? n : 1;
-  k<<<grid, kBulkThreads, smem, s>>>(p->d_chunks, n, bt, wa, wb, sig);
+  SignalArgs sg = sig;
+  sg.l2_hint = g_l2_hint.load();
+  k<<<grid, kBulkThreads, smem, s>>>(p->d_chunks, n, bt, wa, wb, sg);
   return NTP_OK;
 }
 
@@ -803,6 +844,11 @@ using namespace ntp;
 extern "C" {
 
 int ntp_set_option(int option, int64_t value) {
+  if (option == NTP_OPT_SYNC_L2) {
+    if (value < 0 || value > 2) return fail(NTP_EINVAL, "L2 hint must be 0, 1 or 2");
+    g_l2_hint.store((int)value);
+    return NTP_OK;
+  }
   if (option == NTP_OPT_PLAN_MIN_CHUNKS) {
     if (value < 0 || value > 1 << 24) return fail(NTP_EINVAL, "bad minimum chunk count");
     g_min_chunks.store(value);
@@ -821,6 +867,7 @@ int ntp_set_option(int option, int64_t value) {
 }
 
 int64_t ntp_get_option(int option) {
+  if (option == NTP_OPT_SYNC_L2) return g_l2_hint.load();
   if (option == NTP_OPT_PLAN_MIN_CHUNKS) return g_min_chunks.load();
   if (option == NTP_OPT_SYNC_MAX_CTAS) return g_max_ctas.load();
   if (option != NTP_OPT_SYNC_KERNEL) return fail(NTP_EINVAL, "unknown option");
