@@ -22,7 +22,8 @@ from .workloads import SHAPES, busiest_bytes, pair_layout
 
 
 def _max(x: float) -> float:
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    on_gpu = dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if on_gpu else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -35,9 +36,18 @@ def run(args):
     # pointed at stderr while this runs, so stdout is the one JSON line
     os.environ["NCCL_DEBUG"] = os.environ.get("NTP_NCCL_DEBUG", os.environ.get("NCCL_DEBUG", "WARN"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    shared = int(os.environ.get("WORLD_SIZE", "1")) > torch.cuda.device_count()
+    if shared:
+        # more processes than GPUs (a functional run of an N-GPU placement on a
+        # smaller box): processes share GPUs round-robin, host group over gloo
+        # (NCCL puts at most one rank on a GPU); the timings are not N-GPU numbers
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, world = dist.get_rank(), dist.get_world_size()
     L = _lib.load()
     if os.environ.get("NTP_SYNC_KERNEL"):  # experiments: 1 LDG, 2 BULK, 3 BULK2
@@ -138,6 +148,9 @@ def run(args):
                "vs_baseline": None, "dtype": dt,
                "data": "synthetic (N(0,1) gradients)",
                "config": workload_config(args.workload, world),
+               **({"shared_gpus": f"{world} processes on {torch.cuda.device_count()} GPUs: a "
+                                  "functional run of the placement, not an N-GPU measurement"}
+                  if shared else {}),
                "placement": {"healthy": list(plc.h_proc), "reduced": list(plc.r_proc),
                              "busiest_gpu_bytes_per_direction": B,
                              "hosted_bytes_rank0": hosted_bytes},

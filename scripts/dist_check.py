@@ -22,6 +22,8 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
+import _procgroup  # noqa: E402
+
 from oracle import oracle as O  # noqa: E402
 from paper_2504_06095_b200.dist import NtpSyncGroup, Placement  # noqa: E402
 from paper_2504_06095_b200.workloads import ModelShape, pair_layout  # noqa: E402
@@ -37,9 +39,7 @@ def main():
     steps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
     launch = sys.argv[5] if len(sys.argv) > 5 else "fused"
     policy = sys.argv[6] if len(sys.argv) > 6 else "split"
-    local = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    local = _procgroup.init()
     rank, world = dist.get_rank(), dist.get_world_size()
     shape = ModelShape("check", hidden=256, ffn=1000, heads=8, layers=3)
     lay = pair_layout(shape, n1, n2)

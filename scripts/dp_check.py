@@ -17,6 +17,8 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
+import _procgroup  # noqa: E402
+
 from oracle import oracle as O  # noqa: E402
 from paper_2504_06095_b200.dist_dp import DpPlacement, NtpDpGroup, NtpDpMultiGroup  # noqa: E402
 
@@ -33,9 +35,7 @@ def main():
     pieces = int(sys.argv[6]) if len(sys.argv) > 6 else 1
     algo = sys.argv[7] if len(sys.argv) > 7 else "nccl"
     os.environ["NCCL_DEBUG"] = "WARN"
-    local = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    local = _procgroup.init()
     rank, world = dist.get_rank(), dist.get_world_size()
     k, h = 3000, 64
     unit = 2 * h

@@ -19,6 +19,8 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
+import _procgroup  # noqa: E402
+
 from paper_2504_06095_b200.dist_reconfig import (DistReconfig, FailureLayout,  # noqa: E402
                                                  failure_placement)
 from paper_2504_06095_b200.shardmap import build_shard_map  # noqa: E402
@@ -71,9 +73,7 @@ def main():
     mode = sys.argv[1] if len(sys.argv) > 1 else "check"
     n1 = int(sys.argv[2]) if len(sys.argv) > 2 else 4
     dead = int(sys.argv[3]) if len(sys.argv) > 3 else n1 - 1
-    local = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    local = _procgroup.init()
     rank, world = dist.get_rank(), dist.get_world_size()
     if mode == "check":
         shape, layers = ModelShape("check", hidden=64, ffn=1000, heads=8, layers=2), 2

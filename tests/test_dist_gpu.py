@@ -80,6 +80,56 @@ def test_eight_gpus_tp4_tp3():
     _run(8, 4, 3, "bf16", 3)
 
 
+def _run_shared(nproc, min_gpus, script, *args):
+    """nproc processes on fewer GPUs (shared round-robin, gloo host group): the
+    N-process placement and signal wiring on a smaller box."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < min_gpus:
+        pytest.skip(f"needs {min_gpus} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29700 + nproc),
+           os.path.join(ROOT, "scripts", script), *map(str, args)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    return r
+
+
+@pytest.mark.parametrize("launch", ["three", "graph", "fused"])
+def test_eight_rank_placement_on_shared_gpus(launch):
+    """BASELINE configs[1]'s 8-GPU placement (TP4 + TP3 on seven ranks, the
+    eighth idle as the failed GPU) as eight processes sharing the box's GPUs:
+    every rank's plans, partners and signals, vs the oracle."""
+    r = _run_shared(8, 2, "dist_check.py", 4, 3, "bf16", 2, launch)
+    assert "PASS" in r.stdout
+
+
+def test_c3_eight_rank_placement_on_shared_gpus():
+    """BASELINE configs[2] (DP=4: three TP2 replicas + one TP1) in its 8-GPU
+    placement, the one-shot R-way peer-memory group, processes sharing GPUs."""
+    r = _run_shared(8, 2, "dp_check.py", 3, 2, 1, "bf16", 2, 1, "multi")
+    assert "PASS" in r.stdout
+
+
+def test_failure_reconfig_eight_rank_placement_on_shared_gpus():
+    """TP4 -> TP3 failure reconfiguration in the 8-process placement (the dead
+    rank's units pulled from the healthy replica), bit-exact, processes sharing GPUs."""
+    r = _run_shared(8, 2, "reconfig_check.py", "check", 4, 3)
+    assert "PASS" in r.stdout
+
+
+def test_eight_rank_bench_on_shared_gpus():
+    """bench.py's N=8 path end to end (re-executed under torchrun, idle rank,
+    e2e pipeline) on a smaller box: one JSON line, marked as shared GPUs."""
+    import json
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "8", "--steps", "3",
+                        "--warmup", "3", "--workload", "mlp-h1024-ffn4096"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 8 and "shared_gpus" in line and line["value"] > 0
+
+
 def _run_script(n, script, *args):
     if not torch.cuda.is_available() or torch.cuda.device_count() < n:
         pytest.skip(f"needs {n} GPUs")
