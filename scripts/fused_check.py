@@ -20,6 +20,8 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
+import _procgroup  # noqa: E402
+
 from oracle import oracle as O  # noqa: E402
 from paper_2504_06095_b200.dist import NtpSyncGroup, Placement  # noqa: E402
 from paper_2504_06095_b200.linear import MlpShard, finish_push, partner_row_map  # noqa: E402
@@ -39,9 +41,7 @@ def main():
     n2 = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     mode = sys.argv[3] if len(sys.argv) > 3 else "red"
     os.environ["NCCL_DEBUG"] = "WARN"
-    local = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    local = _procgroup.init()
     rank, world = dist.get_rank(), dist.get_world_size()
     h, k, tok_h = 256, 1000, 512
     tok_r = tok_h * n2 // n1

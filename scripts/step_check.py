@@ -18,6 +18,8 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
+import _procgroup  # noqa: E402
+
 from oracle import oracle as O  # noqa: E402
 from paper_2504_06095_b200.dist import NtpSyncGroup, Placement  # noqa: E402
 from paper_2504_06095_b200.linear import MlpShard  # noqa: E402
@@ -30,9 +32,7 @@ def main():
     n2 = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     L = int(sys.argv[3]) if len(sys.argv) > 3 else 3
     os.environ["NCCL_DEBUG"] = "WARN"
-    local = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    local = _procgroup.init()
     rank, world = dist.get_rank(), dist.get_world_size()
     h, k, tok = 256, 1200, 512
     lay = pair_layout(ModelShape("stepcheck", h, k, 0, 1), n1, n2)
@@ -105,7 +105,7 @@ def main():
                 worst = max(worst, O.rel_err(da, want_a), O.rel_err(db, want_b))
         ok &= worst <= 2e-2
         print(f"oracle worst rel err {worst:.3e}", flush=True)
-    t = torch.tensor([int(ok)], device="cuda")
+    t = torch.tensor([int(ok)], device="cpu" if _procgroup.shared() else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MIN)
     if rank == 0:
         print(("PASS" if t.item() else "FAIL") + f" world={world} n1={n1} n2={n2} layers={L}",

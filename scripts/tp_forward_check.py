@@ -11,6 +11,7 @@ layout: "comp" (healthy TP-N columns of build_shard_map(k, N, N-1)) or
 "sync" (the degraded replica's contiguous columns of build_shard_map(k, N+1, N))
 """
 
+import hashlib
 import os
 import sys
 
@@ -19,6 +20,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
+
+import _procgroup  # noqa: E402
 
 from oracle import oracle as O  # noqa: E402
 from paper_2504_06095_b200.dist_linear import TpMlpForward  # noqa: E402
@@ -32,9 +35,7 @@ def main():
     T = int(sys.argv[3]) if len(sys.argv) > 3 else 512
     out_dtype = {"f32": torch.float32, "bf16": torch.bfloat16}[sys.argv[4] if len(sys.argv) > 4 else "f32"]
     os.environ["NCCL_DEBUG"] = "WARN"
-    local = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    local = _procgroup.init()
     rank, n = dist.get_rank(), dist.get_world_size()
     h, k = 256, 1000
     if layout == "comp":
@@ -53,9 +54,10 @@ def main():
         assert tp.status() == 0, "signal timeout"
         want = O.mlp_forward_dense(X, A, B)
         err = O.rel_err(Z.double().cpu().numpy(), want)  # <= 2e-2 (bf16 operands)
-        allz = [torch.empty_like(Z) for _ in range(n)]
-        dist.all_gather(allz, Z)
-        same = all(torch.equal(allz[0], z) for z in allz)
+        digest = hashlib.sha256(Z.cpu().view(torch.uint8).numpy().tobytes()).hexdigest()
+        allz = [None] * n
+        dist.all_gather_object(allz, digest)   # bit-identical Z on every rank
+        same = all(z == allz[0] for z in allz)
         ok &= err <= 2e-2 and same
         if rank == 0:
             print(f"tp_forward n={n} {mode} {layout} T={T} {out_dtype} iter={it} rel_err={err:.3e} "

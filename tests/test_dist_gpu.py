@@ -1,4 +1,10 @@
-"""Multi-GPU sync over IPC peer memory (needs >= 2 GPUs; skipped otherwise)."""
+"""Multi-process sync over IPC peer memory.
+
+Each case runs its N processes on N GPUs; on a box with fewer GPUs the
+processes share them round-robin (scripts/_procgroup.py: gloo host group, the
+device path unchanged), so every placement also runs on a 1-GPU box.  Cases
+that need NCCL itself (the aligned NCCL fall-through, the NCCL DP>2 composition,
+the NCCL TP-forward baseline) need N GPUs and skip otherwise."""
 
 import os
 import subprocess
@@ -12,9 +18,15 @@ from conftest import ROOT
 pytestmark = pytest.mark.gpu
 
 
-def _run(n, *args):
-    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
-        pytest.skip(f"needs {n} GPUs")
+def _need(n, nccl):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    if nccl and torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs (NCCL: one rank per GPU)")
+
+
+def _run(n, *args, nccl=False):
+    _need(n, nccl)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(29500 + n),
            os.path.join(ROOT, "scripts", "dist_check.py"), *map(str, args)]
@@ -53,13 +65,13 @@ def test_two_gpus_step_launch_variants(launch, policy):
 def test_two_gpus_aligned_nccl_fallthrough(n1, dtype):
     """n1 == n2: shards line up, and NtpSyncGroup(aligned="nccl") syncs each
     rank pair with a weighted NCCL all-reduce; same result as the oracle."""
-    _run(2, n1, n1, dtype, 2, "nccl")
+    _run(2, n1, n1, dtype, 2, "nccl", nccl=True)
 
 
 def test_two_gpus_aligned_nccl_prescaled():
     """prescaled=True: the weights were folded into the producer (wgrad alpha);
     the aligned sync is a plain NCCL SUM (no weighting pass)."""
-    _run(2, 4, 4, "f32", 1, "nccl_pre")
+    _run(2, 4, 4, "f32", 1, "nccl_pre", nccl=True)
 
 
 @pytest.mark.parametrize("launch,policy", [("graph", "split"), ("graph_fused", "split"),
@@ -98,21 +110,21 @@ def test_eight_rank_placement_on_shared_gpus(launch):
     """BASELINE configs[1]'s 8-GPU placement (TP4 + TP3 on seven ranks, the
     eighth idle as the failed GPU) as eight processes sharing the box's GPUs:
     every rank's plans, partners and signals, vs the oracle."""
-    r = _run_shared(8, 2, "dist_check.py", 4, 3, "bf16", 2, launch)
+    r = _run_shared(8, 1, "dist_check.py", 4, 3, "bf16", 2, launch)
     assert "PASS" in r.stdout
 
 
 def test_c3_eight_rank_placement_on_shared_gpus():
     """BASELINE configs[2] (DP=4: three TP2 replicas + one TP1) in its 8-GPU
     placement, the one-shot R-way peer-memory group, processes sharing GPUs."""
-    r = _run_shared(8, 2, "dp_check.py", 3, 2, 1, "bf16", 2, 1, "multi")
+    r = _run_shared(8, 1, "dp_check.py", 3, 2, 1, "bf16", 2, 1, "multi")
     assert "PASS" in r.stdout
 
 
 def test_failure_reconfig_eight_rank_placement_on_shared_gpus():
     """TP4 -> TP3 failure reconfiguration in the 8-process placement (the dead
     rank's units pulled from the healthy replica), bit-exact, processes sharing GPUs."""
-    r = _run_shared(8, 2, "reconfig_check.py", "check", 4, 3)
+    r = _run_shared(8, 1, "reconfig_check.py", "check", 4, 3)
     assert "PASS" in r.stdout
 
 
@@ -120,8 +132,8 @@ def test_eight_rank_bench_on_shared_gpus():
     """bench.py's N=8 path end to end (re-executed under torchrun, idle rank,
     e2e pipeline) on a smaller box: one JSON line, marked as shared GPUs."""
     import json
-    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
-        pytest.skip("needs 2 GPUs")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "8", "--steps", "3",
                         "--warmup", "3", "--workload", "mlp-h1024-ffn4096"],
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
@@ -130,9 +142,8 @@ def test_eight_rank_bench_on_shared_gpus():
     assert line["n_gpus"] == 8 and "shared_gpus" in line and line["value"] > 0
 
 
-def _run_script(n, script, *args):
-    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
-        pytest.skip(f"needs {n} GPUs")
+def _run_script(n, script, *args, nccl=False):
+    _need(n, nccl)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(29600 + n),
            os.path.join(ROOT, "scripts", script), *map(str, args)]
@@ -146,7 +157,7 @@ def _run_script(n, script, *args):
 def test_four_gpus_dp3_with_degraded_replica(dtype, pieces):
     """DP=3: two healthy TP2 replicas (one GPU each) + a TP1 replica; pieces > 1
     pipelines fold-in / NCCL all-reduce / push-back on three streams."""
-    _run_script(4, "dp_check.py", 2, 2, 1, dtype, 2, pieces)
+    _run_script(4, "dp_check.py", 2, 2, 1, dtype, 2, pieces, nccl=True)
 
 
 @pytest.mark.parametrize("pieces,algo", [(1, "nccl"), (4, "nccl"), (1, "multi")])
@@ -154,12 +165,12 @@ def test_four_gpus_dp3_with_degraded_replica(dtype, pieces):
 def test_four_gpus_c3_shape(pieces, algo, dtype):
     """BASELINE configs[2] shape on 4 GPUs: DP=4 (3 x TP2 + 1 x TP1), through
     NCCL among the healthy replicas or one R-way peer-memory kernel."""
-    _run_script(4, "dp_check.py", 3, 2, 1, dtype, 2, pieces, algo)
+    _run_script(4, "dp_check.py", 3, 2, 1, dtype, 2, pieces, algo, nccl=algo == "nccl")
 
 
 def test_eight_gpus_c3():
     """BASELINE configs[2]: DP=4 x TP2 with one replica degraded to TP1 (7 GPUs)."""
-    _run_script(8, "dp_check.py", 3, 2, 1, "bf16", 2)
+    _run_script(8, "dp_check.py", 3, 2, 1, "bf16", 2, nccl=True)
 
 
 @pytest.mark.parametrize("mode", ["red", "push", "push_tma", "red_tma"])
@@ -179,14 +190,14 @@ def test_row_parallel_forward_multi_gpu(n, mode, layout, tokens):
     epilogue pushes partial-sum boxes to the row-block owners over NVLink,
     owner sums in rank order, peer gather; vs the fp64 oracle (<= 2e-2) and
     bit-identical on every rank."""
-    _run_script(n, "tp_forward_check.py", mode, layout, tokens)
+    _run_script(n, "tp_forward_check.py", mode, layout, tokens, nccl=mode == "nccl")
 
 
 @pytest.mark.parametrize("n,mode", [(2, "push"), (4, "push"), (2, "nccl")])
 def test_row_parallel_forward_bf16_partials(n, mode):
     """out_dtype=bf16: bf16 partial sums and Z (half the all-reduce bytes), the
     owner still accumulates in fp32; <= 2e-2 of the oracle, identical on every rank."""
-    _run_script(n, "tp_forward_check.py", mode, "sync", 512, "bf16")
+    _run_script(n, "tp_forward_check.py", mode, "sync", 512, "bf16", nccl=mode == "nccl")
 
 
 @pytest.mark.parametrize("n,n1,dead", [(1, 4, 3), (2, 4, 1), (4, 2, 0)])
