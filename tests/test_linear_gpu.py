@@ -37,17 +37,23 @@ def _mk(rows, cols, mn, g):
     return torch.randn((rows, cols), generator=g, device="cuda").to(torch.bfloat16)
 
 
-@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 256), (300, 4779, 200),
-                                   (1366, 1024, 1000), (1, 8, 8), (130, 136, 72)])
-@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def _pitch_ok(M, N, K, a_mn, b_mn):
+    """TMA needs 16-byte row pitches: an MN-major operand's pitch is its M (N)
+    extent, a K-major one's is K (bf16: multiples of 8 elements)."""
+    return not ((a_mn and M % 8) or (b_mn and N % 8) or (not a_mn and K % 8)
+                or (not b_mn and K % 8))
+
+
+_SHAPES = [(128, 256, 64), (256, 512, 256), (300, 4779, 200), (1366, 1024, 1000), (1, 8, 8),
+           (130, 136, 72)]
+_LAYOUTS = [(0, 0), (1, 0), (0, 1), (1, 1)]
+_CASES = [s + l for s in _SHAPES for l in _LAYOUTS if _pitch_ok(*s, *l)]
+_BAD = [s + l for s in _SHAPES for l in _LAYOUTS if not _pitch_ok(*s, *l)]
+
+
+@pytest.mark.parametrize("M,N,K,a_mn,b_mn", _CASES)
 def test_gemm_all_layouts(Lin, M, N, K, a_mn, b_mn):
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N * 3 + K + a_mn * 2 + b_mn)
-    if a_mn and M % 8:
-        pytest.skip("MN-major needs a 16-byte row pitch")
-    if b_mn and N % 8:
-        pytest.skip("MN-major needs a 16-byte row pitch")
-    if not a_mn and K % 8 or not b_mn and K % 8:
-        pytest.skip("K-major needs a 16-byte row pitch")
     A = _mk(M, K, a_mn, g)
     B = _mk(N, K, b_mn, g)
     want = A.float() @ B.float().T
@@ -58,6 +64,16 @@ def test_gemm_all_layouts(Lin, M, N, K, a_mn, b_mn):
     outb = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
     Lin.mm(A, B, outb, alpha=0.5)
     assert rel(outb.float(), 0.5 * want) < 5e-3
+
+
+@pytest.mark.parametrize("M,N,K,a_mn,b_mn", _BAD[:4])
+def test_gemm_rejects_unaligned_pitch(Lin, M, N, K, a_mn, b_mn):
+    """Operands whose row pitch is not a multiple of 16 bytes are refused with a
+    ValueError (TMA cannot map them), never computed wrongly."""
+    g = torch.Generator(device="cuda").manual_seed(1)
+    A, B = _mk(M, K, a_mn, g), _mk(N, K, b_mn, g)
+    with pytest.raises(ValueError, match="16-byte"):
+        Lin.mm(A, B, torch.empty((M, N), dtype=torch.float32, device="cuda"))
 
 
 def test_gemm_epilogues_and_pitch(Lin):
