@@ -343,13 +343,9 @@ def run_e2e_single(args, lay, plan, dtype, eb):
     from paper_2504_06095_b200.workloads import layer_pieces
     lpp = int(os.environ.get("NTP_E2E_LAYERS_PER_PIECE", "1"))
     spp = int(os.environ.get("NTP_E2E_SEGS_PER_PIECE", "0")) or None
-    if len(lay.segs) >= 8:   # pipeline per layer
-        pieces = layer_pieces(lay, dtype, 0, layers_per_piece=lpp, segs_per_piece=spp)
-    else:                    # too few layers (C1): blocks of units
-        from paper_2504_06095_b200.workloads import unit_pieces
-        pieces = unit_pieces(lay, dtype, 0, splits=max(1, 8 // len(lay.segs)))
     hs = HostSync(plan, [e for e in lay.h_elems + lay.r_elems], dtype, device=0,
-                  piece_plans=pieces,
+                  piece_plans=layer_pieces(lay, dtype, 0, layers_per_piece=lpp,
+                                           segs_per_piece=spp),
                   back_to_back=True)  # the timed loop re-runs the same host buffers
     gen = torch.Generator().manual_seed(1)
     host = [torch.randn(e, generator=gen, dtype=torch.float32).to(dtype).pin_memory()

@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .plans import Plan, dtype_code, layout_offsets
+from .plans import Plan, dtype_code
 from .shardmap import build_shard_map
 from .tpnumerics import build_pair_plan
 
@@ -132,33 +132,4 @@ def layer_pieces(lay: PairLayout, dtype, device: int, layers_per_piece: int = 1,
                 hi = int(last[4 + side][a]) + len(last[2 + side][a]) * last[1]
                 ranges.append((a + side * n1, lo, hi))
         pieces.append((plan, ranges))
-    return pieces
-
-
-def unit_pieces(lay: PairLayout, dtype, device: int, splits: int):
-    """Like layer_pieces, but each segment is further cut into `splits` blocks
-    of consecutive columns (units), for workloads too small to pipeline by
-    layer (C1: one MLP).  A block of consecutive columns is a contiguous range
-    of every rank's arena, because each rank stores its columns in ascending
-    order (comp and sync layouts alike)."""
-    pieces = []
-    n1 = lay.n1
-    for k, unit, hc, rc, hb, rb in lay.segs:
-        h_owner, h_off = layout_offsets(hc, k, unit, hb)
-        r_owner, r_off = layout_offsets(rc, k, unit, rb)
-        for b in range(splits):
-            c0, c1 = k * b // splits, k * (b + 1) // splits
-            if c1 <= c0:
-                continue
-            sel = np.arange(c0, c1)
-            plan = Plan(dtype_code(dtype))
-            plan.add_units(unit, h_owner[sel], h_off[sel], n1 + r_owner[sel], r_off[sel])
-            plan = plan.finalize().upload(device)
-            ranges = []
-            for side, (owner, off, count) in enumerate(((h_owner, h_off, n1), (r_owner, r_off, lay.n2))):
-                for a in range(count):
-                    o = off[sel][owner[sel] == a]
-                    if len(o):
-                        ranges.append((a + side * n1, int(o.min()), int(o.max()) + unit))
-            pieces.append((plan, ranges))
     return pieces

@@ -80,28 +80,3 @@ def test_check_reports_out_of_bounds_and_overlap():
     with pytest.raises(ValueError, match="write overlapping elements of buffer 0"):
         q.check([128, 128], write_sides=3)
     q.check([128, 128], write_sides=2)  # side A only read: a copy plan may share sources
-
-
-@pytest.mark.parametrize("shape,n1,n2,splits", [(C1, 4, 3, 8), (C1, 4, 2, 5),
-                                                (ModelShape("o", 64, 601, 6, 1), 5, 3, 3)])
-def test_unit_pieces_tile_every_arena(shape, n1, n2, splits, monkeypatch):
-    """workloads.unit_pieces (the e2e pipeline of one-layer workloads): every
-    piece's plan is in bounds and race free, its arena ranges are exactly its
-    units, and the pieces tile every arena once."""
-    import torch
-    from paper_2504_06095_b200 import workloads as W
-    monkeypatch.setattr(Plan, "upload", lambda self, device: self)  # host-only check
-    lay = pair_layout(shape, n1, n2)
-    elems = list(lay.h_elems) + list(lay.r_elems)
-    cover = [np.zeros(e, dtype=np.int64) for e in elems]
-    for plan, ranges in W.unit_pieces(lay, torch.float32, 0, splits):
-        plan.check(elems)
-        touched = [np.zeros(e, dtype=bool) for e in elems]
-        for ab, ao, bb, bo, ln in plan.export():
-            touched[ab][ao:ao + ln] = True
-            touched[bb][bo:bo + ln] = True
-        for a, lo, hi in ranges:
-            cover[a][lo:hi] += 1
-            assert touched[a][lo:hi].all()
-        assert sum(t.sum() for t in touched) == sum(hi - lo for _, lo, hi in ranges)
-    assert all((c == 1).all() for c in cover)
