@@ -335,6 +335,68 @@ def check_pair_arenas(hidden, ffn, heads, layers, plan, arenas, dtype, h_elems, 
     return res
 
 
+def _segment_input(slot: int, seg: int, n: int, dtype):
+    """Deterministic N(0,1) input of one logical rank's slice of one segment
+    (CPU, any process can regenerate any slot's values)."""
+    import torch
+    g = torch.Generator().manual_seed(1_000_003 * (slot + 1) + seg)
+    return torch.randn(n, generator=g).to(dtype)
+
+
+def check_dist(args, grp, lay, dtype, _max):
+    """--check at N>1: the exact bench plans, every segment of every layer vs
+    the fp64 oracle.  Every arena is refilled with per-(slot, segment) seeded
+    values, ONE step runs, and each process checks the slots it hosts: it
+    regenerates every slot's inputs of a segment on the CPU, runs the oracle's
+    nonuniform_grad_sync (tpnumerics.py:289-356) and compares its own device
+    outputs (Frobenius per segment).  Max over processes."""
+    import torch
+    import torch.distributed as dist
+    from oracle import oracle as O
+    rank = dist.get_rank()
+    hidden, ffn, heads = lay.shape.hidden, lay.shape.ffn, lay.shape.heads
+    segs, _, _ = O.pair_layout(hidden, ffn, heads, lay.layers, lay.n1, lay.n2)
+    n1 = lay.n1
+    nslots = n1 + lay.n2
+
+    def slot_range(seg, s):
+        k, unit, comp, sync, hc, rc, hb, rb = seg
+        cols, base = (hc[s], hb[s]) if s < n1 else (rc[s - n1], rb[s - n1])
+        return int(base), int(base) + len(cols) * unit
+    for i, seg in enumerate(segs):
+        for s in grp.hosted:
+            lo, hi = slot_range(seg, s)
+            grp.arena(s)[lo:hi].copy_(_segment_input(s, i, hi - lo, dtype))
+    torch.cuda.synchronize()
+    dist.barrier()
+    grp.step(W_H, W_R)
+    torch.cuda.synchronize()
+    dist.barrier()
+    worst, t0 = 0.0, time.perf_counter()
+    for i, seg in enumerate(segs):
+        if not grp.hosted:
+            break
+        ins = [_segment_input(s, i, slot_range(seg, s)[1] - slot_range(seg, s)[0], dtype)
+               .double().numpy() for s in range(nslots)]
+        k, unit, comp, sync, hc, rc, hb, rb = seg
+        hw, rw = ins[:n1], ins[n1:]
+        O.nonuniform_sync(comp, sync, hc, rc, hw, rw, unit, op=O.OP_WEIGHTED, weights=(W_H, W_R))
+        want = hw + rw
+        for s in grp.hosted:
+            lo, hi = slot_range(seg, s)
+            got = grp.arena(s)[lo:hi].double().cpu().numpy()
+            worst = max(worst, O.rel_err(got, want[s]))
+    worst = _max(worst)
+    tol = {torch.bfloat16: 2e-2, torch.float32: 1e-6}[dtype]
+    res = {"ok": worst <= tol, "segments": len(segs), "max_rel_err": worst, "tol": tol,
+           "seconds": round(_max(time.perf_counter() - t0), 1),
+           "oracle": "oracle.nonuniform_sync fp64 on the same rounded inputs; every process "
+                     "checks the logical ranks it hosts"}
+    if not res["ok"]:
+        raise RuntimeError(f"bench --check failed at N={dist.get_world_size()}: {res} (rank {rank})")
+    return res
+
+
 def run_e2e_single(args, lay, plan, dtype, eb):
     """Same metric through the public host-buffer API: pinned host arenas in,
     H2D + sync + D2H inside the timed region."""
@@ -532,7 +594,7 @@ def main(argv=None):
                     help="N>1: launch every step eagerly instead of as one CUDA-graph launch")
     ap.add_argument("--check", action="store_true",
                     help="after the timed region, check every segment of one more step "
-                         "against the fp64 oracle (N=1)")
+                         "against the fp64 oracle")
     args = ap.parse_args(argv)
     if args.workload not in WORKLOADS:
         ap.error(f"--workload must be one of {sorted(WORKLOADS)}")

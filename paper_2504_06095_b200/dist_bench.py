@@ -141,6 +141,10 @@ def run(args):
     achieved = B / (ms * 1e-3) / 1e9
     out = None
     e2e = run_e2e(args, grp, lay, dtype, eb)
+    check = None
+    if getattr(args, "check", False):  # the checker lives in bench.py (it runs the oracle)
+        from bench import check_dist  # noqa: I001
+        check = check_dist(args, grp, lay, dtype, _max)
     if rank == 0:
         out = {"metric": METRIC, "value": round(S * eb / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
                "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
@@ -171,6 +175,8 @@ def run(args):
                "timing_detail": timing_detail,
                "gpu_launches": args.steps * _launches_per_step(grp),
                "clocks": clk, "e2e": e2e}
+        if check is not None:
+            out["check"] = check
     dist.barrier()
     grp.close()
     dist.barrier()

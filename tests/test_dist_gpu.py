@@ -135,11 +135,12 @@ def test_eight_rank_bench_on_shared_gpus():
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "8", "--steps", "3",
-                        "--warmup", "3", "--workload", "mlp-h1024-ffn4096"],
+                        "--warmup", "3", "--workload", "mlp-h1024-ffn4096", "--check"],
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 8 and "shared_gpus" in line and line["value"] > 0
+    assert line["check"]["ok"] and line["check"]["max_rel_err"] <= 1e-6  # fp32 C1 vs oracle
 
 
 def _run_script(n, script, *args, nccl=False):
