@@ -266,9 +266,14 @@ int ntp_plan_finalize(ntp_plan *p) {
   for (const Run &r : p->runs) {
     const int64_t g = r.len / grain;
     const int64_t pieces = (g + chunk - 1) / chunk;
+    // split on 8-element boundaries when the run allows it, so the same units
+    // cut at the same elements in every dtype (grains are 2, 4 or 8 elements)
+    const int64_t q = (vectorized && r.len % 8 == 0) ? 8 / grain : 1;
+    const int64_t gq = g / q;
     for (int64_t c = 0; c < pieces; ++c) {
       // near-equal pieces so a long run does not leave a tiny tail chunk
-      const int64_t lo = g * c / pieces, hi = g * (c + 1) / pieces;
+      const int64_t lo = gq * c / pieces * q, hi = gq * (c + 1) / pieces * q;
+      if (hi <= lo) continue;
       const int64_t ao = r.a_off / grain + lo, bo = r.b_off / grain + lo;
       if (ao + (hi - lo) > UINT32_MAX || bo + (hi - lo) > UINT32_MAX)
         return fail(NTP_EINVAL, "buffer offset exceeds the 32-bit grain range of a plan");

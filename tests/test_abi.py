@@ -118,3 +118,20 @@ def test_options_round_trip():
     assert L.ntp_set_option(1, 0) == 0 and L.ntp_get_option(1) == 0
     assert L.ntp_set_option(0, 9) == _lib.NTP_EINVAL
     assert L.ntp_set_option(7, 1) == _lib.NTP_EINVAL
+    # NTP_OPT_PLAN_MIN_CHUNKS (default 1184 = 8 per SM) and NTP_OPT_SYNC_L2 (default 0)
+    assert L.ntp_get_option(2) == 1184 and L.ntp_get_option(3) == 0
+    assert L.ntp_set_option(2, 0) == 0 and L.ntp_get_option(2) == 0
+    assert L.ntp_set_option(2, 1184) == 0
+    assert L.ntp_set_option(3, 3) == _lib.NTP_EINVAL and L.ntp_set_option(2, -1) == _lib.NTP_EINVAL
+    assert L.ntp_gemm_get_max_ctas() == 0
+
+
+def test_min_chunks_splits_small_plans_alike_in_every_dtype():
+    """Small plans get >= 1184 chunks; the chunk size is set in elements, so the
+    same units split identically in bf16, fp32 and fp64."""
+    import torch
+    from paper_2504_06095_b200.workloads import ModelShape, build_plan, pair_layout
+    lay = pair_layout(ModelShape("s", 1024, 1024, 0, 1), 4, 3)
+    tabs = [build_plan(lay, dt).export() for dt in (torch.bfloat16, torch.float32, torch.float64)]
+    assert len(tabs[0]) >= 1184
+    assert all(np.array_equal(tabs[0], t) for t in tabs[1:])
