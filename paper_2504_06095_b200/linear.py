@@ -135,6 +135,18 @@ def partner_row_map(cols, partner_cols, device):
     return (torch.from_numpy(owner[cols]).to(device), torch.from_numpy(pos[cols]).to(device))
 
 
+_NO_PARTNER: dict = {}
+
+
+def _no_partner_rows(M: int, device) -> tuple:
+    """(red_buf, red_row) row maps with no partner copy (-1), cached per (M, device)."""
+    key = (M, str(device))
+    if key not in _NO_PARTNER:
+        _NO_PARTNER[key] = (torch.full((M,), -1, dtype=torch.int32, device=device),
+                            torch.zeros((M,), dtype=torch.int32, device=device))
+    return _NO_PARTNER[key]
+
+
 def _pad8(n: int) -> int:
     return (n + 7) // 8 * 8
 
@@ -167,7 +179,14 @@ class MlpShard:
         T = X.shape[0]
         self.activations(X)
         Y = self.Y[:, :self.n]
-        if accumulate:
+        if accumulate and self.h % 32 == 0 and Z.dtype == torch.float32 and Z.is_contiguous():
+            # Z += Y B_i inside the GEMM: the epilogue adds each staged box into Z
+            # with a TMA bulk reduction (ntp_gemm_bf16_red mode 3, no partner
+            # copy: every row's partner index is -1).  Each element gets one
+            # add, so the ordered sum is exactly Z + part, as the eager add was.
+            rb, rr = _no_partner_rows(T, X.device)
+            mm_red(Y, self.W[:, 1, :].T, Z, 1.0, rb, rr, [], self.h, mode="red_tma")
+        elif accumulate:
             part = torch.empty((T, self.h), dtype=torch.float32, device=X.device)
             mm(Y, self.W[:, 1, :].T, part)
             Z += part

@@ -146,9 +146,10 @@ def test_bf16_replica_backward_runs_tcgen05(T, smaps):
     smap = smaps(k, 4, 3)
     x, g = rng.standard_normal((2, 256, hidden))
     calls = []
-    orig = linear.mm
+    orig, orig_red = linear.mm, linear.mm_red
     monkey = pytest.MonkeyPatch()
     monkey.setattr(linear, "mm", lambda *a, **kw: calls.append(1) or orig(*a, **kw))
+    monkey.setattr(linear, "mm_red", lambda *a, **kw: calls.append(1) or orig_red(*a, **kw))
     try:
         for assignment in (T.assignment_from_comp(smap), T.assignment_from_sync(smap)):
             rep = T.MlpReplica(layer, assignment, dtype=torch.bfloat16)
