@@ -545,7 +545,9 @@ class NtpSyncGroup:
         the step's kernels run back to back.  Same kernels, signals and
         results as step(); each process must issue the same sequence of steps
         (graph or not) so that epochs pair up.  prologue: optional callable
-        recorded before each step (e.g. a benchmark's L2 flush)."""
+        recorded before each step (e.g. a benchmark's L2 flush).  Recording a new
+        graph synchronizes the device once (torch.cuda.graph); replays do not.
+        The graphs hold the group's plans: set_policy()/upload() drop them."""
         if self.aligned == "nccl":
             for _ in range(steps):
                 self.step(w_h, w_r, stream, piece=piece)
