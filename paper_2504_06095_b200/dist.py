@@ -41,7 +41,6 @@ import torch.distributed as dist
 
 from . import _lib
 from .plans import OPS, Plan, dtype_code
-from .tpnumerics import build_pair_plan
 from .workloads import PairLayout
 
 SIG_WORDS = 64             # per page: ready[64] then done[64] (uint64), slot = writer's world rank

@@ -18,7 +18,7 @@ import torch.distributed as dist
 
 from . import _lib
 from .dist import NtpSyncGroup, Placement
-from .workloads import SHAPES, busiest_bytes, pair_layout
+from .workloads import SHAPES, pair_layout
 
 
 def _max(x: float) -> float:

@@ -9,7 +9,6 @@ import pytest
 import torch
 
 from oracle import oracle as O
-from paper_2504_06095_b200 import _lib
 from paper_2504_06095_b200.reconfig import (
     build_reconfig_plan, layouts_for_failure, ownership_after,
 )
